@@ -1,0 +1,314 @@
+#!/usr/bin/env python3
+"""Benchmark of the hot path: Q(f,f) evaluations/s at d=3 N=64 N̄=8 (fp64),
+BASELINE.json's metric, on config c5 (512 spatial cells of perturbed
+Maxwellians per GPU, batched in one dvm_collide_batched call).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU)
+
+A step = one full evaluation of all 512 cells of this rank (all 2017
+directions).  Multi-GPU: cells are sharded by rank (weak scaling: every rank
+owns 512 cells of a global batch of 512*N, no data-path collective), timed on
+the device between barriers, max over ranks.  Inputs (1 GiB per rank) are
+larger than the 126 MB L2, so no explicit flush is needed between steps.
+
+`--impl reference` times the CPU oracle (oracle/, the slow direct pair sum)
+on a bounded sample of the same workload on the host cores (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Q(f,f) evals/sec at d=3 N=64 N̄=8, fp64; achieved HBM GB/s vs peak"
+UNIT = "evals/s"
+D, NGRID, NBAR, L = 3, 64, 8, 8.0
+CELLS_PER_RANK = 512
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            pk = json.load(fh)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                      "-i", str(self.idx)], capture_output=True, text=True, timeout=5).stdout
+                for line in out.strip().splitlines():
+                    self.rows.append([c.strip() for c in line.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for k, n in enumerate(names):
+                if len(r) > 5 + k and r[5 + k].lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_baseline(seconds: float = 15.0):
+    """Oracle (oracle/dvm_oracle.c, as it stands) on a bounded sample of c5:
+    the first cells of the batch, a seeded set of nodes per cell; extrapolated
+    to cell-evaluations/s = (nodes/s) / N^3."""
+    import dvm_inputs
+    from oracle import oracle
+    nodes = NGRID ** D
+    f = dvm_inputs.make("c5", cells=2)
+    Nt = oracle.ntilde_rule(NGRID, NBAR)
+    rng = np.random.default_rng(0)
+    cores = os.cpu_count() or 1
+    # calibrate, then size the sample for ~`seconds` of CPU work
+    pts = rng.integers(0, nodes, size=max(8, cores)).astype(np.int64)
+    t0 = time.perf_counter()
+    oracle.collide(f[0], D, NGRID, NBAR, Nt, L, points=pts)
+    dt = time.perf_counter() - t0
+    n = int(max(cores, min(4 * nodes, len(pts) * seconds / max(dt, 1e-3))))
+    pts = np.sort(rng.integers(0, nodes, size=n)).astype(np.int64)
+    t0 = time.perf_counter()
+    oracle.collide(f[1], D, NGRID, NBAR, Nt, L, points=pts)
+    dt = time.perf_counter() - t0
+    return {"value": (n / dt) / nodes, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{n} seeded nodes of c5 cell 1 (of 64^3), direct pair sum "
+                      f"({oracle.pairs(D, Nt, NBAR, 1.0)[2].size} pairs/node), {dt:.1f} s; "
+                      f"evals/s = nodes/s / 64^3"}
+
+
+def run_reference(args):
+    world, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    import dvm_inputs
+    from oracle import oracle
+    nodes = NGRID ** D
+    Nt = oracle.ntilde_rule(NGRID, NBAR)
+    f = dvm_inputs.make("c5", cells=1)[0]
+    cores = os.cpu_count() or 1
+    rng = np.random.default_rng(1)
+    # each step: a bounded sample of nodes (sized so the whole run takes ~minutes)
+    per_step = int(os.environ.get("REF_NODES_PER_STEP", str(max(8 * cores, 64))))
+    for _ in range(args.warmup):
+        oracle.collide(f, D, NGRID, NBAR, Nt, L, points=rng.integers(0, nodes, size=min(per_step, 16)))
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        pts = np.sort(rng.integers(0, nodes, size=per_step)).astype(np.int64)
+        oracle.collide(f, D, NGRID, NBAR, Nt, L, points=pts)
+    dt = time.perf_counter() - t0
+    value = args.steps * per_step / dt / nodes
+    ms_per_step = dt / args.steps * 1e3 * (nodes / per_step)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded, dvm_inputs c5)",
+            "config": {"workload": "c5: d=3 hard spheres N=64 Nbar=8 Ntilde=14 L=8, evaluation of one cell",
+                       "sample_nodes_per_step": per_step},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"{per_step} seeded nodes of one c5 cell per step, extrapolated: "
+                                       "evals/s = nodes/s / 64^3"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import dvm_inputs
+    from paper_1201_3986_b200 import Plan
+
+    world, rank, local = _dist()
+    if world != args.gpus:
+        print(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    cells = args.cells
+    nodes = NGRID ** D
+    # this rank's shard of the global batch (cells rank*cells ... ), weak scaling
+    f_host = dvm_inputs.make("c5", cells=cells, first_cell=rank * cells)
+    f = torch.from_numpy(f_host).cuda()
+    Q = torch.empty_like(f)
+    plan = Plan(D, NGRID, NBAR)
+    A = plan.A
+    stream = torch.cuda.current_stream()
+
+    for _ in range(args.warmup):
+        plan.collide(f, Q)
+    torch.cuda.synchronize()
+    mass_rel = float((Q.sum(dim=1).abs() / Q.abs().sum(dim=1)).max())
+
+    # ---- headline: device-resident inputs, K steps between barriers, CUDA events
+    launches0 = plan.launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            plan.collide(f, Q)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    launches = plan.launches() - launches0
+    ms_total = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms_total], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    value = world * cells * args.steps / (ms_total / 1e3)
+
+    # ---- dominant kernel: per-launch CUDA events inside libdvm on the same stream
+    plan.profile(True)
+    psteps = max(1, min(args.steps, 2))
+    for _ in range(psteps):
+        plan.collide(f, Q)
+    prof = plan.profile_read()
+    plan.profile(False)
+    prof_total = sum(v[0] for v in prof.values())
+    top = max(prof.items(), key=lambda kv: kv[1][0])
+    top_name, (top_ms, top_n) = top
+    # algorithmic bytes per launch of the dominant kernel: the streaming
+    # formulation charges 8 N^3 bytes per (cell, direction);
+    # one k_rowsum launch processes one direction for all cells of the batch.
+    per_launch_units = cells * (plan.info()["A_local"] / max(1, prof["k_rowsum"][1] / psteps))
+    alg_bytes = 8.0 * nodes * per_launch_units
+    avg_launch_s = top_ms / top_n / 1e3
+    peak, peak_src = _peaks()
+    achieved = alg_bytes / avg_launch_s / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic_per_launch.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(top_name)
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "kernel": top_name, "kernel_share_of_step": top_ms / prof_total,
+                "kernel_avg_launch_ms": top_ms / top_n, "algorithmic_bytes_per_launch": alg_bytes,
+                "peak_source": peak_src,
+                "note": "streaming-formulation bytes (A+2)*8*N^3 per cell-evaluation (SURVEY.md 8(d)); "
+                        "effective, not DRAM traffic"}
+    eff_step_gbs = value / world * (A + 2) * 8.0 * nodes / 1e9
+
+    # ---- e2e through the C ABI with host buffers (pinned), copies inside the timed region
+    fh = torch.from_numpy(f_host).pin_memory()
+    qh = torch.empty_like(fh).pin_memory()
+    plan.collide_host_ptr(fh.data_ptr(), qh.data_ptr(), cells)  # warm (allocates staging)
+    e2e_steps = max(1, min(args.steps, 3))
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        plan.collide_host_ptr(fh.data_ptr(), qh.data_ptr(), cells)
+    t1 = time.perf_counter()
+    e2e_ms = (t1 - t0) * 1e3
+    if world > 1:
+        t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = world * cells * e2e_steps / (e2e_ms / 1e3)
+    same = bool(torch.equal(qh, Q.cpu()))
+
+    clocks = clk.summary()
+    line = None
+    if rank == 0:
+        cpu = cpu_baseline() if (world == 1 and not args.no_cpu_baseline) else None
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded c5 Maxwellian cells, dvm_inputs)",
+                "config": {"workload": "c5: d=3 hard spheres, N=64, Nbar=8, Ntilde=14, L=8, batched cells",
+                           "cells_per_rank": cells, "global_cells": cells * world, "directions": A,
+                           "parallelism": f"cell-sharded x{world}", "l2_flush": "inputs 1 GiB/rank > 126 MB L2",
+                           "effective_streaming_GBps_per_gpu": eff_step_gbs},
+                "roofline": roofline, "cpu_baseline": cpu,
+                "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(fh.numel() * 8),
+                        "d2h_bytes_per_step": int(qh.numel() * 8), "matches_device_result": same},
+                "gpu_launches": int(launches), "clocks": clocks,
+                "checks": {"mass_rel_max": mass_rel},
+                "kernel_profile_ms": {k: v[0] / psteps for k, v in prof.items() if v[1]}}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cells", type=int, default=CELLS_PER_RANK)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("note: --warmup raised to 3 (timing rules)", file=sys.stderr)
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

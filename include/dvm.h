@@ -1,0 +1,178 @@
+/*
+ * dvm.h -- C ABI of libdvm: B200-native (sm_100a, fp64) evaluation of the fast
+ * periodized discrete-velocity Boltzmann collision operator D^{Ñ,N̄}(f,f) of
+ * Mouhot, Pareschi & Rey, arXiv 1201.3986.
+ *
+ * Operation (identical, up to fp64 rounding order, to oracle/dvm_oracle.c):
+ *
+ *   Q_i = sum_{e in A^{d-1}_{N̄}} a_e [ S_e(i) T_e(i) - f_i U_e(i) ]        eq:decD
+ *   S_e(i) = sum_{1<=|m|<=M_e} f_{i+me}              (k-line factor alpha_p)
+ *   T_e(i) = sum_{l in e^⊥, |l|_inf<=Ñ} f_{i+l}       (perp factor alpha'_p)
+ *   U_e(i) = sum_{l in e^⊥, |l|_inf<=Ñ} S_e(i+l)
+ *   a_e = h^{d+1}|e|_2  (= a(me) for every m, a(k) = h^{d+1}|k|/gcd(k))
+ *   M_e = floor(Ñ / |e|_inf),  h = 2L/N,  indices periodic mod N
+ *
+ * A^{d-1}_{N̄} is the set of canonical primitive directions e (gcd 1, first
+ * nonzero component > 0) with |e|_inf <= N̄ -- the "primal representants" of
+ * lines of order N̄.  The sum equals the
+ * direct pair sum of eq:DR restricted to k on those lines; with N̄ = Ñ it is
+ * eq:DR exactly.
+ *
+ * Grid and layout: N points per axis (reading R1), node j <-> v = (j - N/2) h,
+ * N a power of two.  Fields are fp64, row-major [cells][N]...[N] (d axes, last
+ * axis fastest); a cell is N^d contiguous doubles (cell_stride elements apart).
+ *
+ * Conventions for every entry point:
+ *   - Ownership: the plan owns its device direction table and workspace;
+ *     dvm_plan_destroy frees them.  f and Q are caller-owned DEVICE pointers
+ *     (except the *_host variants), 8-byte aligned (16 B recommended).
+ *   - Streams: calls are asynchronous and stream-ordered on the plan's stream
+ *     (params.stream, a cudaStream_t passed as void*; NULL = legacy default
+ *     stream); the *_host variants synchronise before returning.
+ *   - Errors: status codes only -- no exceptions cross the ABI, nothing aborts.
+ *     Asynchronous device faults surface as DVM_E_CUDA at the next call that
+ *     synchronises (or dvm_sync).  dvm_last_error() returns a human-readable
+ *     message for the last failure on the calling thread.
+ *   - Threading: one host thread per plan at a time; distinct plans are
+ *     independent.
+ *   - Determinism: for a fixed plan, input and device the result is bitwise
+ *     reproducible (no floating-point atomics on the accumulation path).
+ */
+#ifndef DVM_H
+#define DVM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DVM_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define DVM_API __attribute__((visibility("default")))
+#else
+#define DVM_API
+#endif
+
+typedef struct dvm_plan_s *dvm_plan_t;
+
+/* Collision kernels with decoupled Heintz-Panferov weights a(k) b(l), b = 1
+ * (PAPER.md:579-587): 2D Maxwell molecules a = h^3|k|/gcd(k1,k2); 3D hard
+ * spheres a = h^5|k|/gcd(k1,k2,k3). */
+typedef enum { DVM_MAXWELL_2D = 0, DVM_HARD_SPHERES_3D = 1 } dvm_kernel_t;
+
+typedef enum {
+    DVM_OK = 0,
+    DVM_E_NULL = 1,        /* a required pointer argument is NULL */
+    DVM_E_DIM = 2,         /* d not in {2,3} */
+    DVM_E_KERNEL = 3,      /* kernel does not match d (Maxwell<->2D, hard spheres<->3D) */
+    DVM_E_ORDER = 4,       /* not 1 <= N̄ <= Ñ, or 2Ñ+1 > N */
+    DVM_E_UNSUPPORTED = 5, /* N not a power of two in [4, 1024] (2D) / [4, 256] (3D); bad L */
+    DVM_E_SHAPE = 6,       /* ncells < 0, cell_stride < N^d, size overflow, bad shard */
+    DVM_E_ALIAS = 7,       /* Q overlaps f */
+    DVM_E_NOMEM = 8,       /* device or host allocation failed */
+    DVM_E_CUDA = 9,        /* CUDA runtime error (incl. asynchronous faults) */
+    DVM_E_STATE = 10       /* call not valid for this plan (e.g. wrong d for dvm_euler moments) */
+} dvm_status_t;
+
+typedef struct {
+    int d;               /* velocity dimension, 2 or 3 */
+    int N;               /* points per axis (power of two) */
+    int Nbar;            /* direction order N̄ >= 1 */
+    int Ntilde;          /* kernel truncation Ñ; 0 -> max(floor(N/(3+sqrt 2)), N̄) (reading R2) */
+    double L;            /* box half-width, h = 2L/N; 0 -> 8.0 (reading R3) */
+    dvm_kernel_t kernel; /* must match d */
+    int device;          /* CUDA device ordinal; -1 -> current device */
+    void *stream;        /* cudaStream_t for all launches; NULL -> default stream */
+    int shard_rank;      /* direction sharding: this plan evaluates only its LPT share */
+    int shard_world;     /*   of the directions (partial Q); 1 -> all directions */
+} dvm_plan_params_t;
+
+typedef struct {
+    int d, N, Nbar, Ntilde, kernel;
+    int A;               /* number of directions in A^{d-1}_{N̄} */
+    int A_local;         /* directions evaluated by this plan (== A unless sharded) */
+    int rows_total;      /* sum over directions of the perp-polygon rows (3D), A (2D) */
+    int64_t nodes;       /* N^d */
+    double L, h;
+    size_t workspace_bytes; /* device bytes currently held by the plan */
+    uint64_t launches;   /* device kernel launches issued by this plan so far */
+} dvm_plan_info_t;
+
+/* Build a plan with Ñ from the rule, L = 8, current device, default stream,
+ * no sharding.  Builds the direction table on the device (K1) and its
+ * per-direction metadata (K2), synchronously.  *out is set only on DVM_OK. */
+DVM_API dvm_status_t dvm_plan(int d, int N, int Nbar, dvm_kernel_t kernel, dvm_plan_t *out);
+
+/* Same with every parameter explicit (see dvm_plan_params_t). */
+DVM_API dvm_status_t dvm_plan_ex(const dvm_plan_params_t *params, dvm_plan_t *out);
+
+DVM_API dvm_status_t dvm_plan_info(dvm_plan_t plan, dvm_plan_info_t *info);
+
+/* Copy the plan's direction table to host arrays (each may be NULL):
+ * dirs[A*d] (canonical e, lexicographic), M[A] (M_e), a[A] (a_e), local[A]
+ * (1 if the direction belongs to this plan's shard). Synchronous. */
+DVM_API dvm_status_t dvm_plan_directions(dvm_plan_t plan, int *dirs, int *M, double *a, int *local);
+
+/* Geometry of direction idx (0 <= idx < A), for inspection and tests: the
+ * row vector u and second basis vector w of e^⊥ ∩ Z^d (3D; 2D: u = e^⊥,
+ * w = 0) and the rows {α u + β w : lo <= α <= hi} of P_e.
+ * u, w receive d ints; b, lo, hi receive up to cap rows; *nrows the count.
+ * Synchronous. */
+DVM_API dvm_status_t dvm_plan_geometry(dvm_plan_t plan, int idx, int *u, int *w, int *nrows, int *b, int *lo,
+                               int *hi, int cap);
+
+/* Change the stream used by subsequent calls (cudaStream_t as void*). */
+DVM_API dvm_status_t dvm_set_stream(dvm_plan_t plan, void *stream);
+
+/* Q = D^{Ñ,N̄}(f,f) for one cell: f, Q device arrays of N^d doubles.  For a
+ * sharded plan, Q is the partial sum over this shard's directions. */
+DVM_API dvm_status_t dvm_collide(dvm_plan_t plan, const double *f, double *Q);
+
+/* Same for ncells cells; cell c occupies [c*cell_stride, c*cell_stride + N^d)
+ * of f and of Q (cell_stride 0 -> N^d). */
+DVM_API dvm_status_t dvm_collide_batched(dvm_plan_t plan, const double *f, double *Q, int64_t ncells,
+                                 int64_t cell_stride);
+
+/* End-to-end variant with HOST buffers: copies f to the device, evaluates and
+ * copies Q back (pinned host memory recommended); synchronous. */
+DVM_API dvm_status_t dvm_collide_batched_host(dvm_plan_t plan, const double *f_host, double *Q_host,
+                                      int64_t ncells, int64_t cell_stride);
+
+/* Moments of one cell (device f): out_host[0] = h^d sum f, out_host[1..d] =
+ * h^d sum v f, out_host[d+1] = h^d sum |v|^2 f (reading R16).  Synchronous,
+ * deterministic. */
+DVM_API dvm_status_t dvm_moments(dvm_plan_t plan, const double *f, double *out_host);
+
+/* Explicit Euler f <- f + dt D(f,f), nsteps times, in place on the device
+ * array f (one cell).  If moments_host != NULL it receives (nsteps+1) rows of
+ * d+2 moments (before the first step and after every step).  Synchronous. */
+DVM_API dvm_status_t dvm_euler(dvm_plan_t plan, double *f, double dt, int nsteps, double *moments_host);
+
+/* Per-kernel timing with CUDA events recorded on the plan's stream around
+ * every launch (for bench.py's roofline; adds one event pair per launch).
+ * enable != 0 clears previous records and starts recording; 0 stops. */
+DVM_API dvm_status_t dvm_profile_enable(dvm_plan_t plan, int enable);
+
+/* Synchronises the plan's stream, then writes, for kernel class k < n, the
+ * summed device time in ms and the launch count of the recorded launches.
+ * Class names: dvm_profile_name(k) (NULL past the last class). */
+DVM_API dvm_status_t dvm_profile_read(dvm_plan_t plan, double *ms, uint64_t *count, int n);
+DVM_API const char *dvm_profile_name(int k);
+
+/* Wait for all work issued on the plan's stream; reports asynchronous faults. */
+DVM_API dvm_status_t dvm_sync(dvm_plan_t plan);
+
+DVM_API dvm_status_t dvm_plan_destroy(dvm_plan_t plan);
+
+DVM_API const char *dvm_status_str(dvm_status_t status);
+DVM_API const char *dvm_last_error(void);
+DVM_API int dvm_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DVM_H */

@@ -1,0 +1,457 @@
+// dvm_api.cu -- the extern "C" entry points of libdvm (include/dvm.h):
+// parameter validation, plan life cycle, host<->device staging, status codes.
+#include <math.h>
+#include <string.h>
+
+#include <new>
+#include <string>
+
+#include "dvm_internal.h"
+
+namespace dvm {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string &msg) { g_last_error = msg; }
+
+dvm_status_t cuda_fail(cudaError_t err, const char *what)
+{
+    g_last_error = std::string(what) + ": " + cudaGetErrorString(err);
+    return DVM_E_CUDA;
+}
+
+}  // namespace dvm
+
+using namespace dvm;
+
+namespace {
+
+bool is_pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
+
+dvm_status_t validate(const dvm_plan_params_t *p, int *Ntilde_out, double *L_out)
+{
+    if (p->d != 2 && p->d != 3) {
+        set_error("d must be 2 or 3");
+        return DVM_E_DIM;
+    }
+    if ((p->d == 2 && p->kernel != DVM_MAXWELL_2D) || (p->d == 3 && p->kernel != DVM_HARD_SPHERES_3D)) {
+        set_error("kernel does not match d (2D Maxwell molecules, 3D hard spheres)");
+        return DVM_E_KERNEL;
+    }
+    const int maxN = p->d == 2 ? 1024 : 256;
+    if (!is_pow2(p->N) || p->N < 4 || p->N > maxN) {
+        set_error("N must be a power of two in [4, 1024] (2D) / [4, 256] (3D)");
+        return DVM_E_UNSUPPORTED;
+    }
+    double L = p->L == 0.0 ? 8.0 : p->L;
+    if (!(L > 0.0) || !isfinite(L)) {
+        set_error("L must be positive and finite");
+        return DVM_E_UNSUPPORTED;
+    }
+    int Nt = p->Ntilde;
+    if (Nt == 0) {  // reading R2: max(floor(N/(3+sqrt 2)), N̄)
+        Nt = (int)floor((double)p->N / (3.0 + sqrt(2.0)));
+        if (Nt < p->Nbar) Nt = p->Nbar;
+    }
+    if (p->Nbar < 1 || p->Nbar > Nt || 2 * Nt + 1 > p->N) {
+        set_error("need 1 <= Nbar <= Ntilde and 2*Ntilde+1 <= N");
+        return DVM_E_ORDER;
+    }
+    if (p->shard_world < 1 || p->shard_rank < 0 || p->shard_rank >= p->shard_world) {
+        set_error("need 0 <= shard_rank < shard_world");
+        return DVM_E_SHAPE;
+    }
+    *Ntilde_out = Nt;
+    *L_out = L;
+    return DVM_OK;
+}
+
+bool overlaps(const double *a, const double *b, int64_t n_a, int64_t n_b)
+{
+    const char *a0 = (const char *)a, *a1 = a0 + n_a * (int64_t)sizeof(double);
+    const char *b0 = (const char *)b, *b1 = b0 + n_b * (int64_t)sizeof(double);
+    return a0 < b1 && b0 < a1;
+}
+
+int64_t nodes_of(const dvm_plan_s *P)
+{
+    int64_t n = 1;
+    for (int j = 0; j < P->d; ++j) n *= P->N;
+    return n;
+}
+
+dvm_status_t check_batch(dvm_plan_s *P, const double *f, double *Q, int64_t ncells, int64_t *stride)
+{
+    if (!P || !f || !Q) {
+        set_error("NULL argument");
+        return DVM_E_NULL;
+    }
+    const int64_t nodes = nodes_of(P);
+    if (*stride == 0) *stride = nodes;
+    if (ncells < 0 || *stride < nodes || (ncells > 0 && *stride > (INT64_MAX / 8) / ncells)) {
+        set_error("bad ncells / cell_stride");
+        return DVM_E_SHAPE;
+    }
+    const int64_t span = ncells > 0 ? (ncells - 1) * *stride + nodes : 0;
+    if (ncells > 0 && overlaps(f, Q, span, span)) {
+        set_error("Q overlaps f");
+        return DVM_E_ALIAS;
+    }
+    return DVM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dvm_abi_version(void) { return DVM_ABI_VERSION; }
+
+const char *dvm_last_error(void) { return g_last_error.c_str(); }
+
+const char *dvm_status_str(dvm_status_t s)
+{
+    switch (s) {
+    case DVM_OK: return "DVM_OK";
+    case DVM_E_NULL: return "DVM_E_NULL: NULL argument";
+    case DVM_E_DIM: return "DVM_E_DIM: d must be 2 or 3";
+    case DVM_E_KERNEL: return "DVM_E_KERNEL: kernel does not match d";
+    case DVM_E_ORDER: return "DVM_E_ORDER: need 1 <= Nbar <= Ntilde, 2 Ntilde + 1 <= N";
+    case DVM_E_UNSUPPORTED: return "DVM_E_UNSUPPORTED: unsupported N or L";
+    case DVM_E_SHAPE: return "DVM_E_SHAPE: bad ncells, cell_stride or shard";
+    case DVM_E_ALIAS: return "DVM_E_ALIAS: Q overlaps f";
+    case DVM_E_NOMEM: return "DVM_E_NOMEM: allocation failed";
+    case DVM_E_CUDA: return "DVM_E_CUDA: CUDA runtime error";
+    case DVM_E_STATE: return "DVM_E_STATE: call not valid for this plan";
+    }
+    return "unknown dvm_status_t";
+}
+
+dvm_status_t dvm_plan_ex(const dvm_plan_params_t *params, dvm_plan_t *out)
+{
+    if (!params || !out) {
+        set_error("NULL argument");
+        return DVM_E_NULL;
+    }
+    int Nt;
+    double L;
+    dvm_status_t st = validate(params, &Nt, &L);
+    if (st) return st;
+    int dev = params->device;
+    if (dev < 0) {
+        cudaError_t e = cudaGetDevice(&dev);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    } else {
+        cudaError_t e = cudaSetDevice(dev);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+    }
+    dvm_plan_s *P = new (std::nothrow) dvm_plan_s();
+    if (!P) {
+        set_error("host allocation failed");
+        return DVM_E_NOMEM;
+    }
+    P->d = params->d;
+    P->N = params->N;
+    P->p = 0;
+    while ((1 << P->p) < P->N) ++P->p;
+    P->Nbar = params->Nbar;
+    P->Ntilde = Nt;
+    P->kernel = params->kernel;
+    P->device = dev;
+    P->L = L;
+    P->h = 2.0 * L / P->N;
+    P->stream = (cudaStream_t)params->stream;
+    P->shard_rank = params->shard_rank;
+    P->shard_world = params->shard_world;
+    P->pk.d = P->d;
+    P->pk.p = P->p;
+    P->pk.N = P->N;
+    P->pk.H = 0;
+    P->pk.mask = 0;
+    for (int j = 0; j < P->d; ++j) {
+        P->pk.H = (P->pk.H << P->p) | (1u << (P->p - 1));
+        P->pk.mask = (P->pk.mask << P->p) | (uint32_t)(P->N - 1);
+    }
+    st = build_table(P);
+    if (st) {
+        free_table(P);
+        delete P;
+        return st;
+    }
+    *out = P;
+    return DVM_OK;
+}
+
+dvm_status_t dvm_plan(int d, int N, int Nbar, dvm_kernel_t kernel, dvm_plan_t *out)
+{
+    dvm_plan_params_t p;
+    memset(&p, 0, sizeof(p));
+    p.d = d;
+    p.N = N;
+    p.Nbar = Nbar;
+    p.Ntilde = 0;
+    p.L = 8.0;
+    p.kernel = kernel;
+    p.device = -1;
+    p.stream = nullptr;
+    p.shard_rank = 0;
+    p.shard_world = 1;
+    return dvm_plan_ex(&p, out);
+}
+
+dvm_status_t dvm_plan_info(dvm_plan_t P, dvm_plan_info_t *info)
+{
+    if (!P || !info) {
+        set_error("NULL argument");
+        return DVM_E_NULL;
+    }
+    info->d = P->d;
+    info->N = P->N;
+    info->Nbar = P->Nbar;
+    info->Ntilde = P->Ntilde;
+    info->kernel = P->kernel;
+    info->A = P->A;
+    info->A_local = (int)P->local.size();
+    info->rows_total = P->R;
+    info->nodes = nodes_of(P);
+    info->L = P->L;
+    info->h = P->h;
+    const Workspace &w = P->ws;
+    info->workspace_bytes = P->table_bytes + sizeof(double) * (w.slots * w.slot_elems * (w.part ? 2 : 1)) +
+                            sizeof(double) * 2 * w.stage_elems;
+    info->launches = P->launches;
+    return DVM_OK;
+}
+
+dvm_status_t dvm_plan_directions(dvm_plan_t P, int *dirs, int *M, double *a, int *local)
+{
+    if (!P) {
+        set_error("NULL argument");
+        return DVM_E_NULL;
+    }
+    for (int i = 0; i < P->A; ++i) {
+        if (dirs)
+            for (int j = 0; j < P->d; ++j) dirs[i * P->d + j] = P->h_e[3 * i + j];
+        if (M) M[i] = P->h_M[i];
+        if (a) a[i] = P->h_a[i];
+        if (local) local[i] = P->is_local[i];
+    }
+    return DVM_OK;
+}
+
+dvm_status_t dvm_plan_geometry(dvm_plan_t P, int idx, int *u, int *w, int *nrows, int *b, int *lo, int *hi,
+                               int cap)
+{
+    if (!P || !nrows) {
+        set_error("NULL argument");
+        return DVM_E_NULL;
+    }
+    if (idx < 0 || idx >= P->A) {
+        set_error("direction index out of range");
+        return DVM_E_SHAPE;
+    }
+    int uu[3], ww[3];
+    DVM_CUDA(cudaMemcpyAsync(uu, P->t.u + 3 * idx, sizeof(uu), cudaMemcpyDeviceToHost, P->stream));
+    DVM_CUDA(cudaMemcpyAsync(ww, P->t.w + 3 * idx, sizeof(ww), cudaMemcpyDeviceToHost, P->stream));
+    const int r0 = P->h_row_off[idx], n = P->h_row_off[idx + 1] - r0;
+    const int m = n < cap ? n : cap;
+    if (m > 0 && b) DVM_CUDA(cudaMemcpyAsync(b, P->t.row_b + r0, sizeof(int) * m, cudaMemcpyDeviceToHost, P->stream));
+    if (m > 0 && lo) DVM_CUDA(cudaMemcpyAsync(lo, P->t.row_lo + r0, sizeof(int) * m, cudaMemcpyDeviceToHost, P->stream));
+    if (m > 0 && hi) DVM_CUDA(cudaMemcpyAsync(hi, P->t.row_hi + r0, sizeof(int) * m, cudaMemcpyDeviceToHost, P->stream));
+    DVM_CUDA(cudaStreamSynchronize(P->stream));
+    for (int j = 0; j < P->d; ++j) {
+        if (u) u[j] = uu[j];
+        if (w) w[j] = ww[j];
+    }
+    *nrows = n;
+    return DVM_OK;
+}
+
+dvm_status_t dvm_set_stream(dvm_plan_t P, void *stream)
+{
+    if (!P) {
+        set_error("NULL argument");
+        return DVM_E_NULL;
+    }
+    P->stream = (cudaStream_t)stream;
+    return DVM_OK;
+}
+
+dvm_status_t dvm_collide_batched(dvm_plan_t P, const double *f, double *Q, int64_t ncells, int64_t cell_stride)
+{
+    dvm_status_t st = check_batch(P, f, Q, ncells, &cell_stride);
+    if (st) return st;
+    return collide_batched(P, f, Q, ncells, cell_stride);
+}
+
+dvm_status_t dvm_collide(dvm_plan_t P, const double *f, double *Q)
+{
+    return dvm_collide_batched(P, f, Q, 1, 0);
+}
+
+dvm_status_t dvm_collide_batched_host(dvm_plan_t P, const double *f_host, double *Q_host, int64_t ncells,
+                                      int64_t cell_stride)
+{
+    dvm_status_t st = check_batch(P, f_host, Q_host, ncells, &cell_stride);
+    if (st) return st;
+    if (ncells == 0) return DVM_OK;
+    const int64_t nodes = nodes_of(P);
+    const size_t elems = (size_t)ncells * nodes;
+    Workspace &w = P->ws;
+    if (w.stage_elems < elems) {
+        DVM_CUDA(cudaStreamSynchronize(P->stream));
+        if (w.f_stage) cudaFree(w.f_stage);
+        if (w.q_stage) cudaFree(w.q_stage);
+        w.f_stage = w.q_stage = nullptr;
+        w.stage_elems = 0;
+        if (cudaMalloc(&w.f_stage, sizeof(double) * elems) != cudaSuccess ||
+            cudaMalloc(&w.q_stage, sizeof(double) * elems) != cudaSuccess) {
+            if (w.f_stage) cudaFree(w.f_stage);
+            w.f_stage = w.q_stage = nullptr;
+            set_error("staging allocation failed");
+            return DVM_E_NOMEM;
+        }
+        w.stage_elems = elems;
+    }
+    if (cell_stride == nodes) {
+        DVM_CUDA(cudaMemcpyAsync(w.f_stage, f_host, sizeof(double) * elems, cudaMemcpyHostToDevice, P->stream));
+    } else {
+        DVM_CUDA(cudaMemcpy2DAsync(w.f_stage, sizeof(double) * nodes, f_host, sizeof(double) * cell_stride,
+                                   sizeof(double) * nodes, ncells, cudaMemcpyHostToDevice, P->stream));
+    }
+    st = collide_batched(P, w.f_stage, w.q_stage, ncells, nodes);
+    if (st) return st;
+    if (cell_stride == nodes) {
+        DVM_CUDA(cudaMemcpyAsync(Q_host, w.q_stage, sizeof(double) * elems, cudaMemcpyDeviceToHost, P->stream));
+    } else {
+        DVM_CUDA(cudaMemcpy2DAsync(Q_host, sizeof(double) * cell_stride, w.q_stage, sizeof(double) * nodes,
+                                   sizeof(double) * nodes, ncells, cudaMemcpyDeviceToHost, P->stream));
+    }
+    DVM_CUDA(cudaStreamSynchronize(P->stream));
+    return DVM_OK;
+}
+
+dvm_status_t dvm_moments(dvm_plan_t P, const double *f, double *out_host)
+{
+    if (!P || !f || !out_host) {
+        set_error("NULL argument");
+        return DVM_E_NULL;
+    }
+    Workspace &w = P->ws;
+    if (!w.mom_dev || w.mom_rows < 1) {
+        if (w.mom_dev) cudaFree(w.mom_dev);
+        DVM_CUDA(cudaMalloc(&w.mom_dev, sizeof(double) * (kMaxD + 2)));
+        w.mom_rows = 1;
+    }
+    dvm_status_t st = moments(P, f, w.mom_dev);
+    if (st) return st;
+    double tmp[kMaxD + 2];
+    DVM_CUDA(cudaMemcpyAsync(tmp, w.mom_dev, sizeof(double) * (kMaxD + 2), cudaMemcpyDeviceToHost, P->stream));
+    DVM_CUDA(cudaStreamSynchronize(P->stream));
+    for (int k = 0; k < P->d + 2; ++k) out_host[k] = tmp[k];
+    return DVM_OK;
+}
+
+dvm_status_t dvm_euler(dvm_plan_t P, double *f, double dt, int nsteps, double *moments_host)
+{
+    if (!P || !f) {
+        set_error("NULL argument");
+        return DVM_E_NULL;
+    }
+    if (nsteps < 0 || !isfinite(dt)) {
+        set_error("bad nsteps / dt");
+        return DVM_E_SHAPE;
+    }
+    const int64_t nodes = nodes_of(P);
+    Workspace &w = P->ws;
+    const size_t rows = (size_t)nsteps + 1;
+    if (!w.mom_dev || w.mom_rows < rows) {
+        DVM_CUDA(cudaStreamSynchronize(P->stream));
+        if (w.mom_dev) cudaFree(w.mom_dev);
+        w.mom_dev = nullptr;
+        DVM_CUDA(cudaMalloc(&w.mom_dev, sizeof(double) * (kMaxD + 2) * rows));
+        w.mom_rows = rows;
+    }
+    if (!w.qtmp) DVM_CUDA(cudaMalloc(&w.qtmp, sizeof(double) * nodes));
+    dvm_status_t st;
+    for (int s = 0; s < nsteps; ++s) {
+        if (moments_host && (st = moments(P, f, w.mom_dev + (size_t)s * (kMaxD + 2)))) return st;
+        if ((st = collide_batched(P, f, w.qtmp, 1, nodes))) return st;
+        if ((st = axpy(P, f, w.qtmp, dt))) return st;
+    }
+    if (moments_host) {
+        if ((st = moments(P, f, w.mom_dev + (size_t)nsteps * (kMaxD + 2)))) return st;
+        std::string buf;
+        buf.resize(sizeof(double) * (kMaxD + 2) * rows);
+        DVM_CUDA(cudaMemcpyAsync(&buf[0], w.mom_dev, buf.size(), cudaMemcpyDeviceToHost, P->stream));
+        DVM_CUDA(cudaStreamSynchronize(P->stream));
+        const double *src = (const double *)buf.data();
+        for (size_t r = 0; r < rows; ++r)
+            for (int k = 0; k < P->d + 2; ++k) moments_host[r * (P->d + 2) + k] = src[r * (kMaxD + 2) + k];
+    } else {
+        DVM_CUDA(cudaStreamSynchronize(P->stream));
+    }
+    return DVM_OK;
+}
+
+dvm_status_t dvm_profile_enable(dvm_plan_t P, int enable)
+{
+    if (!P) {
+        set_error("NULL argument");
+        return DVM_E_NULL;
+    }
+    DVM_CUDA(cudaStreamSynchronize(P->stream));
+    clear_profile(P);
+    P->profiling = enable != 0;
+    return DVM_OK;
+}
+
+static const char *kClassNames[] = {"k_linesum", "k_rowsum", "k_reduce", "k_zero", "k_moments", "k_axpy", "plan"};
+
+const char *dvm_profile_name(int k) { return (k >= 0 && k < KC_COUNT) ? kClassNames[k] : nullptr; }
+
+dvm_status_t dvm_profile_read(dvm_plan_t P, double *ms, uint64_t *count, int n)
+{
+    if (!P || !ms || !count) {
+        set_error("NULL argument");
+        return DVM_E_NULL;
+    }
+    DVM_CUDA(cudaStreamSynchronize(P->stream));
+    for (int k = 0; k < n; ++k) {
+        ms[k] = 0.0;
+        count[k] = 0;
+    }
+    for (auto &r : P->prof) {
+        if (r.cls >= n) continue;
+        float t = 0.f;
+        DVM_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+        ms[r.cls] += t;
+        count[r.cls] += 1;
+    }
+    return DVM_OK;
+}
+
+dvm_status_t dvm_sync(dvm_plan_t P)
+{
+    if (!P) {
+        set_error("NULL argument");
+        return DVM_E_NULL;
+    }
+    DVM_CUDA(cudaStreamSynchronize(P->stream));
+    DVM_CUDA(cudaGetLastError());
+    return DVM_OK;
+}
+
+dvm_status_t dvm_plan_destroy(dvm_plan_t P)
+{
+    if (!P) {
+        set_error("NULL argument");
+        return DVM_E_NULL;
+    }
+    cudaStreamSynchronize(P->stream);
+    free_workspace(P);
+    free_table(P);
+    delete P;
+    return DVM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,151 @@
+// dvm_internal.h -- private declarations of libdvm (product code; never shared with oracle/).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/dvm.h"
+
+namespace dvm {
+
+constexpr int kMaxD = 3;
+
+// Packed node index: the row-major linear index of a node, viewed as d fields
+// of p = log2(N) bits (axis 0 most significant).  Adding two packed vectors
+// component-wise modulo N is a carry-less SWAR add (swar_add); this is how the
+// periodic wrap of PAPER.md:383-385 is applied to every stencil offset.
+struct Packing {
+    int d, p, N;
+    uint32_t H;     // top bit of every field
+    uint32_t mask;  // all fields
+};
+
+__host__ __device__ inline uint32_t swar_add(uint32_t a, uint32_t b, uint32_t H)
+{
+    return ((a & ~H) + (b & ~H)) ^ ((a ^ b) & H);
+}
+
+__host__ __device__ inline uint32_t pack_vec(const int *c, int d, int p, int N)
+{
+    uint32_t r = 0;
+    for (int j = 0; j < d; ++j) {
+        int m = c[j] % N;
+        if (m < 0) m += N;
+        r = (r << p) | (uint32_t)m;
+    }
+    return r;
+}
+
+// Device-resident direction table (struct of arrays, A directions, R rows).
+struct DirTable {
+    int *e = nullptr;        // [A*3] canonical primitive direction (unused comps 0)
+    int *M = nullptr;        // [A] M_e = floor(Ñ/|e|_inf)
+    double *a = nullptr;     // [A] a_e = h^{d+1} |e|_2
+    int *u = nullptr;        // [A*3] row vector of the perp polygon (2D: e^⊥)
+    int *w = nullptr;        // [A*3] second basis vector of e^⊥ ∩ Z^3 (2D: 0)
+    int *nrows = nullptr;    // [A]
+    int *row_off = nullptr;  // [A+1] CSR offsets into rows
+    int *cost = nullptr;     // [A] work estimate (LPT sharding)
+    int *row_b = nullptr;    // [R]
+    int *row_lo = nullptr;   // [R]
+    int *row_hi = nullptr;   // [R]
+    uint32_t *off_in = nullptr;     // [R] packed (hi_b+1) u + b w
+    uint32_t *off_out = nullptr;    // [R] packed lo_b u + b w (also the row start)
+    int *local = nullptr;           // [A_local] direction indices of this plan's shard
+};
+
+struct Workspace {
+    double *S = nullptr;     // [slots][cells][nodes] line sums S_e
+    double *part = nullptr;  // [slots][cells][nodes] per-direction contributions
+    size_t slot_elems = 0;   // cells*nodes capacity per slot
+    int slots = 0;
+    double *f_stage = nullptr, *q_stage = nullptr;  // host e2e staging
+    size_t stage_elems = 0;
+    double *mom_partial = nullptr;  // [kMomBlocks][kMaxD+2]
+    double *mom_dev = nullptr;      // [(steps+1)][kMaxD+2]
+    size_t mom_rows = 0;
+    double *qtmp = nullptr;         // euler scratch (nodes)
+};
+
+}  // namespace dvm
+
+namespace dvm {
+enum KernelClass { KC_LINESUM = 0, KC_ROWSUM, KC_REDUCE, KC_ZERO, KC_MOMENTS, KC_AXPY, KC_PLAN, KC_COUNT };
+struct ProfRec {
+    int cls;
+    cudaEvent_t a, b;
+};
+}  // namespace dvm
+
+struct dvm_plan_s {
+    int d, N, p, Nbar, Ntilde, kernel, device;
+    double L, h;
+    cudaStream_t stream;
+    int A = 0, R = 0;
+    int shard_rank = 0, shard_world = 1;
+    dvm::Packing pk;
+    dvm::DirTable t;
+    // host mirrors (small)
+    std::vector<int> h_e, h_M, h_nrows, h_row_off, h_cost;
+    std::vector<double> h_a;
+    std::vector<int> local;      // direction indices evaluated by this plan, ascending
+    std::vector<uint8_t> is_local;
+    dvm::Workspace ws;
+    uint64_t launches = 0;
+    size_t table_bytes = 0;
+    bool profiling = false;
+    std::vector<dvm::ProfRec> prof;
+};
+
+namespace dvm {
+
+// Launch bookkeeping: counts every launch; with profiling on, brackets it
+// with CUDA events on the plan's stream.
+struct LaunchScope {
+    dvm_plan_s *P;
+    ProfRec rec;
+    bool on;
+    LaunchScope(dvm_plan_s *p, int cls) : P(p), on(p->profiling)
+    {
+        ++P->launches;
+        if (on) {
+            rec.cls = cls;
+            cudaEventCreate(&rec.a);
+            cudaEventCreate(&rec.b);
+            cudaEventRecord(rec.a, P->stream);
+        }
+    }
+    ~LaunchScope()
+    {
+        if (on) {
+            cudaEventRecord(rec.b, P->stream);
+            P->prof.push_back(rec);
+        }
+    }
+};
+void clear_profile(dvm_plan_s *P);
+
+// error reporting (thread-local message)
+void set_error(const std::string &msg);
+dvm_status_t cuda_fail(cudaError_t err, const char *what);
+
+#define DVM_CUDA(call)                                                   \
+    do {                                                                 \
+        cudaError_t _e = (call);                                         \
+        if (_e != cudaSuccess) return ::dvm::cuda_fail(_e, #call);       \
+    } while (0)
+
+// plan construction (dvm_plan.cu)
+dvm_status_t build_table(dvm_plan_s *P);
+void free_table(dvm_plan_s *P);
+
+// evaluation (dvm_collide.cu)
+dvm_status_t collide_batched(dvm_plan_s *P, const double *f, double *Q, int64_t ncells, int64_t stride);
+dvm_status_t moments(dvm_plan_s *P, const double *f, double *dev_out_row);
+dvm_status_t axpy(dvm_plan_s *P, double *f, const double *q, double dt);
+void free_workspace(dvm_plan_s *P);
+
+}  // namespace dvm

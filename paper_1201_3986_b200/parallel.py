@@ -1,0 +1,70 @@
+"""Multi-GPU plumbing (one process per GPU, torch.distributed).
+
+Two shardings of the hot path (the decomposition eq:decD is
+a sum over directions and the operator is local in x, so both are exact):
+
+* direction sharding of ONE grid (c1-c4): rank r evaluates the LPT share of
+  the directions (libdvm's dvm_plan_ex shard_rank/shard_world) into a partial
+  Q_r, then one fp64 sum all-reduce over NVLink (NCCL) gives Q = sum_r Q_r;
+* cell sharding of a batch (c5): contiguous blocks of cells per rank, no
+  collective on the data path.
+
+The compute step is injected (`partial_fn`) so that the same reduction code
+path runs in the CPU `gloo` tests with the oracle standing in for the GPU
+kernel (tests only) and on the GPU with libdvm.
+"""
+from __future__ import annotations
+
+from typing import Callable, Sequence
+
+import numpy as np
+
+
+def cell_range(ncells: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous block of cells owned by `rank`: (first, count); remainders to low ranks."""
+    if world < 1 or not 0 <= rank < world or ncells < 0:
+        raise ValueError("bad cell sharding arguments")
+    base, rem = divmod(ncells, world)
+    first = rank * base + min(rank, rem)
+    return first, base + (1 if rank < rem else 0)
+
+
+def lpt_assign(costs: Sequence[int], world: int) -> np.ndarray:
+    """Owner rank of every direction: longest-processing-time first, ties to the
+    lowest rank, stable in direction order.  Mirrors libdvm's build_table."""
+    costs = np.asarray(costs, dtype=np.int64)
+    order = sorted(range(len(costs)), key=lambda i: (-costs[i], i))
+    load = np.zeros(world, dtype=np.int64)
+    owner = np.zeros(len(costs), dtype=np.int64)
+    for i in order:
+        r = int(np.argmin(load))
+        load[r] += costs[i]
+        owner[i] = r
+    return owner
+
+
+def sharded_collide(partial_fn: Callable, f, group=None):
+    """Q = all_reduce_sum(partial_fn(f)) over the process group.
+
+    partial_fn(f) returns this rank's partial Q (a torch tensor on the rank's
+    device: CUDA + NCCL in production, CPU + gloo in tests)."""
+    import torch.distributed as dist
+    q = partial_fn(f)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(q, op=dist.ReduceOp.SUM, group=group)
+    return q
+
+
+class DirectionSharded:
+    """Direction-sharded evaluation of one grid on this rank's GPU."""
+
+    def __init__(self, d: int, N: int, Nbar: int, group=None, **plan_kw):
+        import torch.distributed as dist
+        from .dvm import Plan
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.group = group
+        self.plan = Plan(d, N, Nbar, shard_rank=rank, shard_world=world, **plan_kw)
+
+    def __call__(self, f, out=None):
+        return sharded_collide(lambda x: self.plan.collide(x, out), f, self.group)

@@ -1,0 +1,281 @@
+"""GPU parity: libdvm (through the C ABI) against the CPU oracle, element by
+element on the same seeded inputs.  Bar (BASELINE.json north_star):
+max|Q_gpu - Q_oracle| <= 1e-11 * max|Q_oracle| in fp64.
+
+Full grids where the oracle finishes in seconds; at BASELINE full sizes
+(c3, c4, c5 in bench.py's launch configuration) on sampled nodes the oracle
+computes one by one (27/9 nodes around argmax f + seeded uniform nodes), plus
+invariants that hold at any size.
+"""
+import itertools
+import math
+
+import numpy as np
+import pytest
+
+import dvm_inputs
+from oracle import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-11
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _plan(d, N, Nbar, **kw):
+    from paper_1201_3986_b200 import Plan
+    return Plan(d, N, Nbar, **kw)
+
+
+def _gpu(plan, f_np):
+    f = torch.from_numpy(np.ascontiguousarray(f_np, dtype=np.float64)).cuda()
+    q = plan.collide(f)
+    torch.cuda.synchronize()
+    return q.cpu().numpy()
+
+
+def _assert_parity(Qg, Qo, what, ref=None):
+    scale = np.abs(Qo).max() if ref is None else ref
+    err = np.abs(Qg - Qo).max()
+    assert err <= TOL * scale, f"{what}: max err {err:.3e} > {TOL:g} * {scale:.3e} (rel {err / scale:.2e})"
+    return err / scale
+
+
+def _sample_points(f_cell, d, N, n_uniform, seed):
+    arg = int(np.argmax(f_cell))
+    c = []
+    r = arg
+    for _ in range(d):
+        c.append(r % N)
+        r //= N
+    c = c[::-1]
+    pts = set()
+    for off in itertools.product((-1, 0, 1), repeat=d):
+        idx = 0
+        for j in range(d):
+            idx = idx * N + (c[j] + off[j]) % N
+        pts.add(idx)
+    rng = np.random.default_rng(seed)
+    pts.update(int(x) for x in rng.integers(0, N ** d, size=n_uniform))
+    return np.array(sorted(pts), dtype=np.int64)
+
+
+# ---------------------------------------------------------------- plan tables
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
+def test_direction_table_matches_definition(name):
+    cfg = dvm_inputs.CONFIGS[name]
+    p = _plan(cfg.d, cfg.N, cfg.Nbar)
+    dirs, M, a, loc = p.directions()
+    assert np.array_equal(dirs, oracle.directions(cfg.d, cfg.Nbar))
+    assert p.Ntilde == oracle.ntilde_rule(cfg.N, cfg.Nbar)
+    inf = np.abs(dirs).max(axis=1)
+    assert np.array_equal(M, p.Ntilde // inf)
+    np.testing.assert_allclose(a, p.h ** (cfg.d + 1) * np.sqrt((dirs.astype(float) ** 2).sum(1)), rtol=1e-15)
+    assert loc.all()
+
+
+@pytest.mark.parametrize("name", ["c2", "c4", "c5"])
+def test_perp_rows_equal_perp_set(name):
+    """The rows {αu+βw : lo<=α<=hi} of every direction are exactly
+    P_e = {l in [-Ñ,Ñ]^d : l.e = 0}, each point once."""
+    cfg = dvm_inputs.CONFIGS[name]
+    p = _plan(cfg.d, cfg.N, cfg.Nbar)
+    Nt = p.Ntilde
+    dirs = p.directions()[0]
+    box = np.array(list(itertools.product(range(-Nt, Nt + 1), repeat=cfg.d)))
+    for i, e in enumerate(dirs):
+        u, w, rows = p.geometry(i)
+        if cfg.d == 3:
+            assert np.array_equal(np.cross(u, w), e)  # basis of e^⊥ ∩ Z^3
+        pts = []
+        for b, lo, hi in rows:
+            for al in range(lo, hi + 1):
+                pts.append(tuple(al * u + b * w))
+        want = {tuple(l) for l in box[box @ e == 0]}
+        assert len(pts) == len(set(pts)) == len(want) and set(pts) == want, (i, e)
+
+
+def test_lpt_sharding_matches_host_logic():
+    from paper_1201_3986_b200 import parallel
+    cfg = dvm_inputs.CONFIGS["c4"]
+    full = _plan(3, cfg.N, cfg.Nbar)
+    costs = [4 * len(full.geometry(i)[2]) + 8 for i in range(full.A)]
+    for world in (2, 3, 8):
+        owner = parallel.lpt_assign(costs, world)
+        for r in range(world):
+            loc = _plan(3, cfg.N, cfg.Nbar, shard_rank=r, shard_world=world).directions()[3]
+            assert np.array_equal(loc, owner == r)
+
+
+# ---------------------------------------------------------------- parity, full grids
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_parity_full_2d(name):
+    cfg = dvm_inputs.CONFIGS[name]
+    f = dvm_inputs.make(name)
+    p = _plan(cfg.d, cfg.N, cfg.Nbar)
+    Qg = _gpu(p, f)
+    Qo, G, _ = oracle.collide(f, cfg.d, cfg.N, cfg.Nbar, p.Ntilde, cfg.L)
+    _assert_parity(Qg, Qo, name)
+    assert abs(Qg.sum()) <= 1e-13 * G.sum()
+
+
+@pytest.mark.parametrize("d,N,Nbar,Nt", [(3, 16, 3, 3), (3, 16, 2, 7), (3, 8, 1, 3), (2, 32, 5, 7),
+                                         (2, 8, 1, 3), (2, 4, 1, 1)])
+def test_parity_full_small(d, N, Nbar, Nt):
+    f = dvm_inputs.two_bumps(d, N, 8.0, 1.5, 0.01, 3).reshape(-1)
+    p = _plan(d, N, Nbar, Ntilde=Nt)
+    Qg = _gpu(p, f)
+    Qo, _, _ = oracle.collide(f, d, N, Nbar, Nt, 8.0)
+    _assert_parity(Qg, Qo, f"d={d} N={N} Nbar={Nbar} Nt={Nt}")
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_parity_fuzz(seed):
+    rng = np.random.default_rng(50 + seed)
+    d = 2 if seed % 2 == 0 else 3
+    N = int(rng.choice([8, 16, 32])) if d == 2 else int(rng.choice([8, 16]))
+    Ntmax = (N - 1) // 2
+    Nt = int(rng.integers(1, Ntmax + 1))
+    Nbar = int(rng.integers(1, Nt + 1))
+    L = float(rng.uniform(1.0, 10.0))
+    cells = int(rng.integers(1, 4))
+    f = rng.uniform(0.0, 1.0, size=(cells, N ** d))
+    p = _plan(d, N, Nbar, Ntilde=Nt, L=L)
+    Qg = _gpu(p, f)
+    Qo, _, _ = oracle.collide(f, d, N, Nbar, Nt, L)
+    for c in range(cells):
+        _assert_parity(Qg[c], Qo[c], f"fuzz seed={seed} cell={c}")
+
+
+# ---------------------------------------------------------------- parity, BASELINE sizes (sampled)
+@pytest.mark.parametrize("name,npts", [("c3", 1500), ("c4", 3000)])
+def test_parity_sampled_single_grid(name, npts):
+    cfg = dvm_inputs.CONFIGS[name]
+    f = dvm_inputs.make(name)
+    p = _plan(cfg.d, cfg.N, cfg.Nbar)
+    Qg = _gpu(p, f)[0]
+    pts = _sample_points(f[0], cfg.d, cfg.N, npts, 7)
+    Qo, G, _ = oracle.collide(f, cfg.d, cfg.N, cfg.Nbar, p.Ntilde, cfg.L, points=pts)
+    _assert_parity(Qg[pts], Qo[0], name)
+    # invariants at full size: exact mass conservation
+    assert abs(Qg.sum()) <= 1e-12 * np.abs(Qg).sum()
+
+
+def test_parity_c5_sampled_batched():
+    """c5 in bench.py's launch configuration (512 cells in one batched call)."""
+    cfg = dvm_inputs.CONFIGS["c5"]
+    f = dvm_inputs.make("c5")
+    p = _plan(3, cfg.N, cfg.Nbar)
+    Qg = _gpu(p, f)
+    cells = [0, 1, 137, 511]
+    for c in cells:
+        pts = _sample_points(f[c], 3, cfg.N, 40, 100 + c)
+        Qo, G, _ = oracle.collide(f[c], 3, cfg.N, cfg.Nbar, p.Ntilde, cfg.L, points=pts)
+        _assert_parity(Qg[c][pts], Qo[0], f"c5 cell {c}")
+    sums = Qg.sum(axis=1)
+    assert np.all(np.abs(sums) <= 1e-12 * np.abs(Qg).sum(axis=1))
+
+
+# ---------------------------------------------------------------- trajectories, invariants
+def test_c2_euler_trajectory():
+    """c2: 100 explicit Euler steps dt = 0.01 (reading R11); Q parity on the GPU
+    state at steps 0, 50, 100; mass drift at round-off."""
+    cfg = dvm_inputs.CONFIGS["c2"]
+    p = _plan(2, 64, 8)
+    f0 = dvm_inputs.make("c2")[0]
+    f = torch.from_numpy(f0.copy()).cuda()
+    moms = []
+    for step in (0, 50, 100):
+        if step:
+            moms.append(p.euler(f, 0.01, 50))
+        fs = f.cpu().numpy()
+        assert fs.min() >= 0.0  # positivity
+        Qg = _gpu(p, fs)
+        Qo, _, _ = oracle.collide(fs, 2, 64, 8, p.Ntilde, 8.0)
+        _assert_parity(Qg[0], Qo[0], f"c2 step {step}")
+    m = np.concatenate([moms[0], moms[1][1:]])
+    assert m.shape == (101, 4)
+    assert abs(m[-1, 0] - m[0, 0]) <= 1e-12 * m[0, 0]
+    # and the moments agree with a host recomputation
+    h = p.h
+    v = (np.arange(64) - 32) * h
+    fs = f.cpu().numpy().reshape(64, 64)
+    np.testing.assert_allclose(m[-1, 0], h * h * fs.sum(), rtol=1e-13)
+    np.testing.assert_allclose(m[-1, 3], h * h * ((v[:, None] ** 2 + v[None, :] ** 2) * fs).sum(), rtol=1e-12)
+
+
+@pytest.mark.parametrize("d,N,Nbar", [(2, 64, 8), (3, 32, 4)])
+def test_constant_field(d, N, Nbar):
+    p = _plan(d, N, Nbar)
+    Q1 = _gpu(p, np.ones(N ** d))
+    assert np.all(Q1 == 0.0)  # every sum is an exact small integer (reading R18)
+    Qc = _gpu(p, np.full(N ** d, 0.3))
+    _, G, _ = oracle.collide(np.full(N ** d, 0.3), d, N, Nbar, p.Ntilde, 8.0, points=np.arange(4))
+    assert np.abs(Qc).max() <= 1e-13 * G.max()
+
+
+def test_determinism_bitwise():
+    cfg = dvm_inputs.CONFIGS["c4"]
+    f = dvm_inputs.make("c4")
+    p = _plan(3, cfg.N, cfg.Nbar)
+    assert np.array_equal(_gpu(p, f), _gpu(p, f))
+    p2 = _plan(3, cfg.N, cfg.Nbar)
+    assert np.array_equal(_gpu(p, f), _gpu(p2, f))
+
+
+@pytest.mark.parametrize("name,world", [("c3", 4), ("c4", 3), ("c1", 8)])
+def test_direction_shards_sum_to_full(name, world):
+    """Sequentially on one GPU: the sum of the shard partials equals the full
+    evaluation (the multi-GPU all-reduce adds exactly these partials)."""
+    cfg = dvm_inputs.CONFIGS[name]
+    f = dvm_inputs.make(name)
+    full = _gpu(_plan(cfg.d, cfg.N, cfg.Nbar), f)
+    acc = np.zeros_like(full)
+    seen = np.zeros(_plan(cfg.d, cfg.N, cfg.Nbar).A, dtype=int)
+    for r in range(world):
+        p = _plan(cfg.d, cfg.N, cfg.Nbar, shard_rank=r, shard_world=world)
+        seen += p.directions()[3]
+        acc += _gpu(p, f)
+    assert np.all(seen == 1)
+    np.testing.assert_allclose(acc, full, rtol=0, atol=1e-13 * np.abs(full).max())
+
+
+def test_host_entry_point_matches_device():
+    cfg = dvm_inputs.CONFIGS["c4"]
+    f = dvm_inputs.make("c4")
+    p = _plan(3, cfg.N, cfg.Nbar)
+    assert np.array_equal(p.collide_host(f), _gpu(p, f))
+
+
+def test_batched_edge_cases():
+    from paper_1201_3986_b200 import DvmError
+    p = _plan(2, 16, 4)
+    f = np.random.default_rng(1).uniform(0, 1, size=(5, 256))
+    Qb = _gpu(p, f)
+    for c in range(5):
+        assert np.array_equal(Qb[c], _gpu(p, f[c])[0])
+    ft = torch.from_numpy(f).cuda()
+    with pytest.raises(DvmError) as ei:
+        p.collide(ft, out=ft)
+    assert ei.value.name == "DVM_E_ALIAS"
+    # zero cells is a no-op
+    import ctypes
+    from paper_1201_3986_b200 import dvm as _d
+    st = _d.load().dvm_collide_batched(p._h, ctypes.c_void_p(ft.data_ptr()),
+                                       ctypes.c_void_p(ft.data_ptr() + 8 * ft.numel()), 0, 0)
+    assert st == 0
+    # strided cells (cell_stride > N^d)
+    big = torch.zeros((5, 300), dtype=torch.float64, device="cuda")
+    big[:, :256] = ft
+    out = torch.full_like(big, 7.0)
+    st = _d.load().dvm_collide_batched(p._h, ctypes.c_void_p(big.data_ptr()), ctypes.c_void_p(out.data_ptr()), 5, 300)
+    assert st == 0
+    torch.cuda.synchronize()
+    o = out.cpu().numpy()
+    assert np.array_equal(o[:, :256], Qb) and np.all(o[:, 256:] == 7.0)
