@@ -196,9 +196,9 @@ def test_c2_euler_trajectory():
             moms.append(p.euler(f, 0.01, 50))
         fs = f.cpu().numpy()
         assert fs.min() >= 0.0  # positivity
-        Qg = _gpu(p, fs)
+        Qg = _gpu(p, fs).reshape(-1)
         Qo, _, _ = oracle.collide(fs, 2, 64, 8, p.Ntilde, 8.0)
-        _assert_parity(Qg[0], Qo[0], f"c2 step {step}")
+        _assert_parity(Qg, Qo[0], f"c2 step {step}")
     m = np.concatenate([moms[0], moms[1][1:]])
     assert m.shape == (101, 4)
     assert abs(m[-1, 0] - m[0, 0]) <= 1e-12 * m[0, 0]
@@ -259,7 +259,7 @@ def test_batched_edge_cases():
     f = np.random.default_rng(1).uniform(0, 1, size=(5, 256))
     Qb = _gpu(p, f)
     for c in range(5):
-        assert np.array_equal(Qb[c], _gpu(p, f[c])[0])
+        assert np.array_equal(Qb[c], _gpu(p, f[c]).reshape(-1))
     ft = torch.from_numpy(f).cuda()
     with pytest.raises(DvmError) as ei:
         p.collide(ft, out=ft)
