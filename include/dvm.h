@@ -162,6 +162,11 @@ DVM_API dvm_status_t dvm_profile_enable(dvm_plan_t plan, int enable);
 DVM_API dvm_status_t dvm_profile_read(dvm_plan_t plan, double *ms, uint64_t *count, int n);
 DVM_API const char *dvm_profile_name(int k);
 
+/* Evaluation path: 0 = default (3D N in {32,64,128}: cluster-per-cell plane
+ * kernel; otherwise orbit sweeps), 1 = orbit sweeps only (v1, cross-checks).
+ * Both compute the same operator; results agree to rounding. */
+DVM_API dvm_status_t dvm_set_path(dvm_plan_t plan, int path);
+
 /* Wait for all work issued on the plan's stream; reports asynchronous faults. */
 DVM_API dvm_status_t dvm_sync(dvm_plan_t plan);
 

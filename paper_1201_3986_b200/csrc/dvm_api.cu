@@ -405,7 +405,8 @@ dvm_status_t dvm_profile_enable(dvm_plan_t P, int enable)
     return DVM_OK;
 }
 
-static const char *kClassNames[] = {"k_linesum", "k_rowsum", "k_reduce", "k_zero", "k_moments", "k_axpy", "plan"};
+static const char *kClassNames[] = {"k_linesum", "k_rowsum", "k_reduce", "k_zero", "k_moments", "k_axpy", "plan",
+                                    "k_cluster3d"};
 
 const char *dvm_profile_name(int k) { return (k >= 0 && k < KC_COUNT) ? kClassNames[k] : nullptr; }
 
@@ -427,6 +428,20 @@ dvm_status_t dvm_profile_read(dvm_plan_t P, double *ms, uint64_t *count, int n)
         ms[r.cls] += t;
         count[r.cls] += 1;
     }
+    return DVM_OK;
+}
+
+dvm_status_t dvm_set_path(dvm_plan_t P, int path)
+{
+    if (!P) {
+        set_error("NULL argument");
+        return DVM_E_NULL;
+    }
+    if (path != 0 && path != 1) {
+        set_error("path must be 0 (default) or 1 (v1 orbit sweeps)");
+        return DVM_E_STATE;
+    }
+    P->force_v1 = path == 1;
     return DVM_OK;
 }
 

@@ -1,0 +1,376 @@
+// dvm_cluster3d.cu -- v2 3D evaluation: one thread-block CLUSTER per cell,
+// persistent over all directions, one launch per collide.
+//
+// For a direction e, let (u, w) be the basis of e^⊥ ∩ Z^3 from the plan and z
+// a transverse vector with z.e = 1, so (u, w, z) is unimodular and every node
+// is x = γ z + α u + β w (mod N) for exactly one (γ, α, β) in Z_N^3: the
+// lattice planes x.e ≡ γ are N×N tori in (α, β).  The perp polygon P_e
+// lies in plane 0 as rows {α u + β w : lo_b <= α <= hi_b},
+// so T_e = Σ_{l∈P_e} f(.+l) is a 2D polygon filter inside each plane, and the
+// line factors are 1D windows along e-orbits.  Per direction:
+//
+//   phase A  each CTA of the cluster takes planes γ = rank, rank+CL, ...:
+//            gathers the plane of f into shared memory as row prefix sums
+//            P(β, α) (warp scans), then T(α, β) = Σ_b [P(β+b, α+hi_b) −
+//            P(β+b, α+lo_b−1)] (+ row total on wrap) and writes T to the
+//            cluster's T buffer (L2-resident, N^3 doubles).
+//   cluster barrier (release/acquire: T visible, L1 invalidated)
+//   phase B  threads sweep e-orbits (sliding windows, as v1): S = window of
+//            f, U = window of T along e, Q(x) += a_e (S T − f U)
+//            (eq:decD; U = Σ_{m≠0} T(.+me) is the loss).
+//   cluster barrier
+//
+// Q accumulates in direction order (bitwise deterministic, no atomics).  Many
+// cells in flight (one per cluster) keep the working set f + T + Q of the
+// cells in flight in L2.  Small batches split each cell's directions into
+// chunks with partial Q buffers reduced afterwards in chunk order.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+
+#include "dvm_internal.h"
+
+namespace cg = cooperative_groups;
+
+namespace dvm {
+namespace {
+
+constexpr int kCT = 1024;      // threads per CTA
+constexpr int kMaxRows = 256;  // perp-polygon rows held in shared memory
+
+struct C3Args {
+    const double *f;
+    int64_t f_stride;
+    double *Q;  // direct target (nchunks == 1) or partial buffer [chunk][cell][N^3]
+    int64_t q_stride;
+    double *Tbuf;  // [clusters][N^3]
+    int64_t ncells;
+    int nchunks;
+    const int *dirs;
+    int ndirs;
+    const int *E, *U, *W, *Z, *M;
+    const double *a;
+    const int *row_off, *row_b, *row_lo, *row_hi;
+    uint32_t H;
+    int p;
+    int seg_len, nseg;
+};
+
+template <int N>
+__device__ __forceinline__ uint32_t pack3(int c0, int c1, int c2, int p)
+{
+    return ((uint32_t)(c0 & (N - 1)) << (2 * p)) | ((uint32_t)(c1 & (N - 1)) << p) | (uint32_t)(c2 & (N - 1));
+}
+
+template <int N>
+__global__ void __launch_bounds__(kCT, 1) k_cluster3d(C3Args A)
+{
+    constexpr int LPL = N / 32;   // row elements per lane in the prefix scan
+    constexpr int OUT = N / 32;   // outputs per thread per axis in phase A
+    constexpr int NW = kCT / 32;  // warps per CTA
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double *sP = reinterpret_cast<double *>(smem_raw);  // [N][N] row prefix sums
+    double *sTot = sP + N * N;                          // [N] row totals
+    int *sB = reinterpret_cast<int *>(sTot + N);
+    int *sLo = sB + kMaxRows;
+    int *sHi = sLo + kMaxRows;
+    __shared__ int s_meta[16];
+
+    cg::cluster_group cluster = cg::this_cluster();
+    const int CL = (int)cluster.num_blocks();
+    const int rank = (int)cluster.block_rank();
+    const int cid = blockIdx.x / CL;
+    const int nclusters = gridDim.x / CL;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int p = A.p;
+    const uint32_t H = A.H;
+    constexpr int NN = N * N;
+    const int64_t nodes = (int64_t)N * N * N;
+    double *Tb = A.Tbuf + (int64_t)cid * nodes;
+    const int64_t items = A.ncells * A.nchunks;
+
+    for (int64_t item = cid; item < items; item += nclusters) {
+        const int64_t cell = item / A.nchunks;
+        const int chunk = (int)(item % A.nchunks);
+        const int d0 = (int)((int64_t)A.ndirs * chunk / A.nchunks);
+        const int d1 = (int)((int64_t)A.ndirs * (chunk + 1) / A.nchunks);
+        const double *fc = A.f + cell * A.f_stride;
+        double *Qc = A.nchunks == 1 ? A.Q + cell * A.q_stride : A.Q + ((int64_t)chunk * A.ncells + cell) * nodes;
+
+        for (int di = d0; di < d1; ++di) {
+            const int dir = A.dirs[di];
+            if (threadIdx.x == 0) {
+                for (int j = 0; j < 3; ++j) {
+                    s_meta[j] = A.E[3 * dir + j];
+                    s_meta[3 + j] = A.U[3 * dir + j];
+                    s_meta[6 + j] = A.W[3 * dir + j];
+                    s_meta[9 + j] = A.Z[3 * dir + j];
+                }
+                s_meta[12] = A.M[dir];
+                s_meta[13] = A.row_off[dir];
+                s_meta[14] = min(A.row_off[dir + 1] - A.row_off[dir], kMaxRows);
+            }
+            __syncthreads();
+            const int r0 = s_meta[13], nr = s_meta[14];
+            for (int k = threadIdx.x; k < nr; k += kCT) {
+                sB[k] = A.row_b[r0 + k];
+                sLo[k] = A.row_lo[r0 + k];
+                sHi[k] = A.row_hi[r0 + k];
+            }
+            const int e0 = s_meta[0], e1 = s_meta[1], e2 = s_meta[2];
+            const int u0 = s_meta[3], u1 = s_meta[4], u2 = s_meta[5];
+            const int w0 = s_meta[6], w1 = s_meta[7], w2 = s_meta[8];
+            const int z0 = s_meta[9], z1 = s_meta[10], z2 = s_meta[11];
+            const int M = s_meta[12];
+            const double aw = A.a[dir];
+            __syncthreads();
+
+            // ---------------- phase A: T on this CTA's planes
+            for (int g = rank; g < N; g += CL) {
+                // row prefix sums of f on plane g (warp per row)
+#pragma unroll
+                for (int i = 0; i < N / NW; ++i) {
+                    const int beta = warp + NW * i;
+                    const int b0 = g * z0 + beta * w0, b1 = g * z1 + beta * w1, b2 = g * z2 + beta * w2;
+                    double v[LPL];
+#pragma unroll
+                    for (int j = 0; j < LPL; ++j) {
+                        const int al = lane * LPL + j;
+                        v[j] = __ldg(fc + pack3<N>(b0 + al * u0, b1 + al * u1, b2 + al * u2, p));
+                    }
+#pragma unroll
+                    for (int j = 1; j < LPL; ++j) v[j] += v[j - 1];
+                    double x = v[LPL - 1];
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        double y = __shfl_up_sync(0xffffffffu, x, o);
+                        if (lane >= o) x += y;
+                    }
+                    const double excl = x - v[LPL - 1];
+#pragma unroll
+                    for (int j = 0; j < LPL; ++j) sP[beta * N + lane * LPL + j] = v[j] + excl;
+                    if (lane == 31) sTot[beta] = x;
+                }
+                __syncthreads();
+                double t[OUT][OUT];
+#pragma unroll
+                for (int gg = 0; gg < OUT; ++gg)
+#pragma unroll
+                    for (int h = 0; h < OUT; ++h) t[gg][h] = 0.0;
+                for (int k = 0; k < nr; ++k) {
+                    const int b = sB[k], lo = sLo[k] - 1, hi = sHi[k];
+#pragma unroll
+                    for (int gg = 0; gg < OUT; ++gg) {
+                        const int rr = (warp + NW * gg + b) & (N - 1);
+                        const double *row = sP + rr * N;
+                        const double tot = sTot[rr];
+#pragma unroll
+                        for (int h = 0; h < OUT; ++h) {
+                            const int al = lane + 32 * h;
+                            const int ah = al + hi, aL = al + lo;
+                            double s = row[ah & (N - 1)] - row[aL & (N - 1)];
+                            const int wrap = (ah >> p) - (aL >> p);
+                            if (wrap) s += (double)wrap * tot;
+                            t[gg][h] += s;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int gg = 0; gg < OUT; ++gg) {
+                    const int beta = warp + NW * gg;
+                    const int b0 = g * z0 + beta * w0, b1 = g * z1 + beta * w1, b2 = g * z2 + beta * w2;
+#pragma unroll
+                    for (int h = 0; h < OUT; ++h) {
+                        const int al = lane + 32 * h;
+                        Tb[pack3<N>(b0 + al * u0, b1 + al * u1, b2 + al * u2, p)] = t[gg][h];
+                    }
+                }
+                __syncthreads();
+            }
+            cluster.sync();
+
+            // ---------------- phase B: e-orbit sweeps -> S, U, Q
+            {
+                const int gt = rank * kCT + threadIdx.x;
+                if (gt < NN * A.nseg) {
+                    const int r = gt % NN, seg = gt / NN;
+                    // transversal axis: first non-fastest odd component of e
+                    const int ja = (e0 & 1) ? 0 : ((e1 & 1) ? 1 : 2);
+                    int c[3];
+                    // insert x_ja = 0 into the 2-field orbit index r
+                    const int hiF = r >> p, loF = r & (N - 1);
+                    if (ja == 0) { c[0] = 0; c[1] = hiF; c[2] = loF; }
+                    else if (ja == 1) { c[0] = hiF; c[1] = 0; c[2] = loF; }
+                    else { c[0] = hiF; c[1] = loF; c[2] = 0; }
+                    const int t0 = seg * A.seg_len;
+                    uint32_t x = pack3<N>(c[0] + t0 * e0, c[1] + t0 * e1, c[2] + t0 * e2, p);
+                    const uint32_t Ev = pack3<N>(e0, e1, e2, p);
+                    const uint32_t Pin = pack3<N>((M + 1) * e0, (M + 1) * e1, (M + 1) * e2, p);
+                    const uint32_t Pout = pack3<N>(-M * e0, -M * e1, -M * e2, p);
+                    double Wf = 0.0, WT = 0.0;
+                    uint32_t y = swar_add(x, Pout, H);
+                    for (int m = -M; m <= M; ++m) {
+                        Wf += __ldg(fc + y);
+                        WT += Tb[y];
+                        y = swar_add(y, Ev, H);
+                    }
+                    for (int s = 0; s < A.seg_len; ++s) {
+                        const double fx = __ldg(fc + x), Tx = Tb[x];
+                        const double S = Wf - fx, Uu = WT - Tx;
+                        Qc[x] += aw * (S * Tx - fx * Uu);
+                        const uint32_t yi = swar_add(x, Pin, H), yo = swar_add(x, Pout, H);
+                        Wf += __ldg(fc + yi) - __ldg(fc + yo);
+                        WT += Tb[yi] - Tb[yo];
+                        x = swar_add(x, Ev, H);
+                    }
+                }
+            }
+            cluster.sync();
+        }
+    }
+}
+
+template <int N>
+size_t smem_bytes()
+{
+    return sizeof(double) * ((size_t)N * N + N) + sizeof(int) * 3 * kMaxRows;
+}
+
+template <int N>
+dvm_status_t launch(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q, int64_t q_stride,
+                    int64_t ncells, bool *handled)
+{
+    auto kern = k_cluster3d<N>;
+    const size_t smem = smem_bytes<N>();
+    DVM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    DVM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    // cluster size: the one keeping the most SMs busy (ties: larger clusters,
+    // fewer cells in flight, smaller L2 working set)
+    int best_cl = 0, best_nc = 0;
+    for (int cl : {16, 8, 4, 2}) {
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = cl;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(cl, 1, 1);
+        cfg.blockDim = dim3(kCT, 1, 1);
+        cfg.dynamicSmemBytes = smem;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int nc = 0;
+        if (cudaOccupancyMaxActiveClusters(&nc, (void *)kern, &cfg) != cudaSuccess) {
+            cudaGetLastError();
+            continue;
+        }
+        if (nc * cl > best_nc * best_cl) {
+            best_cl = cl;
+            best_nc = nc;
+        }
+    }
+    if (best_cl == 0) {
+        *handled = false;
+        return DVM_OK;
+    }
+    const int nloc = (int)P->local.size();
+    const int64_t nodes = (int64_t)N * N * N;
+    int nchunks = 1;
+    if (ncells < best_nc) nchunks = (int)std::min<int64_t>(nloc, (best_nc + ncells - 1) / ncells);
+    const int64_t items = ncells * nchunks;
+    const int nclusters = (int)std::min<int64_t>(best_nc, items);
+    Workspace &w = P->ws;
+    const size_t need_T = (size_t)nclusters * nodes;
+    const size_t need_part = nchunks > 1 ? (size_t)nchunks * ncells * nodes : 0;
+    if (w.c3_T_elems < need_T || w.c3_part_elems < need_part) {
+        DVM_CUDA(cudaStreamSynchronize(P->stream));
+        if (w.c3_T) cudaFree(w.c3_T);
+        if (w.c3_part) cudaFree(w.c3_part);
+        w.c3_T = w.c3_part = nullptr;
+        w.c3_T_elems = w.c3_part_elems = 0;
+        if (cudaMalloc(&w.c3_T, sizeof(double) * need_T) != cudaSuccess ||
+            (need_part && cudaMalloc(&w.c3_part, sizeof(double) * need_part) != cudaSuccess)) {
+            set_error("cluster workspace allocation failed");
+            return DVM_E_NOMEM;
+        }
+        w.c3_T_elems = need_T;
+        w.c3_part_elems = need_part;
+    }
+    C3Args a;
+    a.f = f;
+    a.f_stride = f_stride;
+    a.Q = nchunks == 1 ? Q : w.c3_part;
+    a.q_stride = nchunks == 1 ? q_stride : nodes;
+    a.Tbuf = w.c3_T;
+    a.ncells = ncells;
+    a.nchunks = nchunks;
+    a.dirs = P->t.local;
+    a.ndirs = nloc;
+    a.E = P->t.e;
+    a.U = P->t.u;
+    a.W = P->t.w;
+    a.Z = P->t.z;
+    a.M = P->t.M;
+    a.a = P->t.a;
+    a.row_off = P->t.row_off;
+    a.row_b = P->t.row_b;
+    a.row_lo = P->t.row_lo;
+    a.row_hi = P->t.row_hi;
+    a.H = P->pk.H;
+    a.p = P->p;
+    int nseg = 1;
+    while (nseg * 2 <= best_cl * kCT / (N * N) && N / (nseg * 2) >= 8) nseg *= 2;
+    a.nseg = nseg;
+    a.seg_len = N / nseg;
+    // zero the accumulation target
+    if (nchunks == 1) {
+        dvm_status_t st = zero_cells(P, Q, q_stride, ncells, nodes);
+        if (st) return st;
+    } else {
+        dvm_status_t st = zero_cells(P, w.c3_part, nodes, (int64_t)nchunks * ncells, nodes);
+        if (st) return st;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = best_cl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(nclusters * best_cl, 1, 1);
+    cfg.blockDim = dim3(kCT, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = P->stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    {
+        LaunchScope ls(P, KC_CLUSTER3D);
+        DVM_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+    }
+    if (nchunks > 1) {
+        dvm_status_t st = zero_cells(P, Q, q_stride, ncells, nodes);
+        if (st) return st;
+        st = reduce_slots(P, Q, q_stride, w.c3_part, (int64_t)ncells * nodes, nchunks, ncells, nodes);
+        if (st) return st;
+    }
+    *handled = true;
+    return DVM_OK;
+}
+
+}  // namespace
+
+dvm_status_t collide_cluster3d(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q, int64_t q_stride,
+                               int64_t ncells, bool *handled)
+{
+    *handled = false;
+    if (P->d != 3 || ncells <= 0 || P->local.empty()) return DVM_OK;
+    for (int i : P->local)
+        if (P->h_nrows[i] > kMaxRows) return DVM_OK;
+    switch (P->N) {
+    case 32: return launch<32>(P, f, f_stride, Q, q_stride, ncells, handled);
+    case 64: return launch<64>(P, f, f_stride, Q, q_stride, ncells, handled);
+    case 128: return launch<128>(P, f, f_stride, Q, q_stride, ncells, handled);
+    default: return DVM_OK;
+    }
+}
+
+}  // namespace dvm

@@ -292,10 +292,32 @@ dvm_status_t ensure_ws(dvm_plan_s *P, int slots, size_t slot_elems, bool need_pa
 
 }  // namespace
 
+dvm_status_t zero_cells(dvm_plan_s *P, double *Q, int64_t q_stride, int64_t ncells, int64_t nodes)
+{
+    LaunchScope ls(P, KC_ZERO);
+    k_zero<<<592, kThreads, 0, P->stream>>>(Q, q_stride, ncells, nodes);
+    DVM_CUDA(cudaGetLastError());
+    return DVM_OK;
+}
+
+dvm_status_t reduce_slots(dvm_plan_s *P, double *Q, int64_t q_stride, const double *part, int64_t slot_elems,
+                          int nslots, int64_t ncells, int64_t nodes)
+{
+    LaunchScope ls(P, KC_REDUCE);
+    k_reduce<<<592, kThreads, 0, P->stream>>>(Q, q_stride, part, slot_elems, nslots, ncells, nodes);
+    DVM_CUDA(cudaGetLastError());
+    return DVM_OK;
+}
+
 dvm_status_t collide_batched(dvm_plan_s *P, const double *f, double *Q, int64_t ncells, int64_t stride)
 {
     const Geo g = geo_of(P);
     if (ncells == 0) return DVM_OK;
+    if (P->d == 3 && !P->force_v1) {
+        bool handled = false;
+        dvm_status_t st = collide_cluster3d(P, f, stride, Q, stride, ncells, &handled);
+        if (st || handled) return st;
+    }
     const int zero_blocks = 592;
     {
         LaunchScope ls(P, KC_ZERO);
@@ -390,7 +412,7 @@ void free_workspace(dvm_plan_s *P)
 {
     clear_profile(P);
     Workspace &w = P->ws;
-    void *ptrs[] = {w.S, w.part, w.f_stage, w.q_stage, w.mom_partial, w.mom_dev, w.qtmp};
+    void *ptrs[] = {w.S, w.part, w.f_stage, w.q_stage, w.mom_partial, w.mom_dev, w.qtmp, w.c3_T, w.c3_part};
     for (void *q : ptrs)
         if (q) cudaFree(q);
     w = Workspace{};

@@ -46,6 +46,7 @@ struct DirTable {
     double *a = nullptr;     // [A] a_e = h^{d+1} |e|_2
     int *u = nullptr;        // [A*3] row vector of the perp polygon (2D: e^⊥)
     int *w = nullptr;        // [A*3] second basis vector of e^⊥ ∩ Z^3 (2D: 0)
+    int *z = nullptr;        // [A*3] transverse vector, z.e = 1: (u, w, z) is unimodular (3D)
     int *nrows = nullptr;    // [A]
     int *row_off = nullptr;  // [A+1] CSR offsets into rows
     int *cost = nullptr;     // [A] work estimate (LPT sharding)
@@ -68,12 +69,15 @@ struct Workspace {
     double *mom_dev = nullptr;      // [(steps+1)][kMaxD+2]
     size_t mom_rows = 0;
     double *qtmp = nullptr;         // euler scratch (nodes)
+    double *c3_T = nullptr;         // v2 cluster kernel: per-cluster T buffers
+    double *c3_part = nullptr;      // v2 cluster kernel: per-chunk partial Q
+    size_t c3_T_elems = 0, c3_part_elems = 0;
 };
 
 }  // namespace dvm
 
 namespace dvm {
-enum KernelClass { KC_LINESUM = 0, KC_ROWSUM, KC_REDUCE, KC_ZERO, KC_MOMENTS, KC_AXPY, KC_PLAN, KC_COUNT };
+enum KernelClass { KC_LINESUM = 0, KC_ROWSUM, KC_REDUCE, KC_ZERO, KC_MOMENTS, KC_AXPY, KC_PLAN, KC_CLUSTER3D, KC_COUNT };
 struct ProfRec {
     int cls;
     cudaEvent_t a, b;
@@ -97,6 +101,7 @@ struct dvm_plan_s {
     uint64_t launches = 0;
     size_t table_bytes = 0;
     bool profiling = false;
+    bool force_v1 = false;  // evaluation path selector (testing): v1 orbit sweeps only
     std::vector<dvm::ProfRec> prof;
 };
 
@@ -146,6 +151,11 @@ void free_table(dvm_plan_s *P);
 dvm_status_t collide_batched(dvm_plan_s *P, const double *f, double *Q, int64_t ncells, int64_t stride);
 dvm_status_t moments(dvm_plan_s *P, const double *f, double *dev_out_row);
 dvm_status_t axpy(dvm_plan_s *P, double *f, const double *q, double dt);
+dvm_status_t zero_cells(dvm_plan_s *P, double *Q, int64_t q_stride, int64_t ncells, int64_t nodes);
+dvm_status_t reduce_slots(dvm_plan_s *P, double *Q, int64_t q_stride, const double *part, int64_t slot_elems,
+                          int nslots, int64_t ncells, int64_t nodes);
+dvm_status_t collide_cluster3d(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q, int64_t q_stride,
+                               int64_t ncells, bool *handled);
 void free_workspace(dvm_plan_s *P);
 
 }  // namespace dvm

@@ -220,9 +220,32 @@ __device__ void perp_basis(const int *e, int Nt, int *u_out, int *w_out)
     }
 }
 
+// z with z.e = 1 (e primitive): Bezout on (a, b) -> g, then on (g, c) -> 1.
+__device__ void transverse(const int *e, int *z)
+{
+    auto egcd = [](long long a, long long b, long long &x, long long &y) {
+        long long r0 = a < 0 ? -a : a, r1 = b < 0 ? -b : b, s0 = 1, s1 = 0, t0 = 0, t1 = 1;
+        while (r1) {
+            long long q = r0 / r1, tmp;
+            tmp = r0 - q * r1; r0 = r1; r1 = tmp;
+            tmp = s0 - q * s1; s0 = s1; s1 = tmp;
+            tmp = t0 - q * t1; t0 = t1; t1 = tmp;
+        }
+        x = a < 0 ? -s0 : s0;
+        y = b < 0 ? -t0 : t0;
+        return r0;
+    };
+    long long s, t, s2, t2;
+    long long g = egcd(e[0], e[1], s, t);   // s e0 + t e1 = g
+    egcd(g, e[2], s2, t2);                   // s2 g + t2 e2 = 1
+    z[0] = (int)(s2 * s);
+    z[1] = (int)(s2 * t);
+    z[2] = (int)t2;
+}
+
 // K2a: one thread per direction.
 __global__ void k_dirmeta(int d, int A, int Nt, double hd1, const int *E, int *M, double *aw, int *U,
-                          int *W, int *nrows, int *cost)
+                          int *W, int *Z, int *nrows, int *cost)
 {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= A) return;
@@ -237,8 +260,9 @@ __global__ void k_dirmeta(int d, int A, int Nt, double hd1, const int *E, int *M
     int m = Nt / inf;
     M[t] = m;
     aw[t] = hd1 * sqrt((double)n2);  // a(me) = h^{d+1}|me|/|m|
-    int u[3] = {0, 0, 0}, w[3] = {0, 0, 0};
+    int u[3] = {0, 0, 0}, w[3] = {0, 0, 0}, z[3] = {0, 0, 0};
     int nr;
+    if (d == 3) transverse(e, z);
     if (d == 2) {
         u[0] = -e[1];
         u[1] = e[0];
@@ -250,6 +274,7 @@ __global__ void k_dirmeta(int d, int A, int Nt, double hd1, const int *E, int *M
     for (int j = 0; j < 3; ++j) {
         U[3 * t + j] = u[j];
         W[3 * t + j] = w[j];
+        Z[3 * t + j] = z[j];
     }
     nrows[t] = nr;
     cost[t] = 4 * nr + 8;
@@ -343,6 +368,7 @@ dvm_status_t build_table(dvm_plan_s *P)
     if ((st = dalloc(&t.a, A, &acc))) return st;
     if ((st = dalloc(&t.u, (size_t)A * 3, &acc))) return st;
     if ((st = dalloc(&t.w, (size_t)A * 3, &acc))) return st;
+    if ((st = dalloc(&t.z, (size_t)A * 3, &acc))) return st;
     if ((st = dalloc(&t.nrows, A, &acc))) return st;
     if ((st = dalloc(&t.row_off, A + 1, &acc))) return st;
     if ((st = dalloc(&t.cost, A, &acc))) return st;
@@ -350,7 +376,7 @@ dvm_status_t build_table(dvm_plan_s *P)
     int blocks = (A + 127) / 128;
     {
         LaunchScope ls(P, KC_PLAN);
-        k_dirmeta<<<blocks, 128, 0, P->stream>>>(d, A, P->Ntilde, hd1, t.e, t.M, t.a, t.u, t.w, t.nrows, t.cost);
+        k_dirmeta<<<blocks, 128, 0, P->stream>>>(d, A, P->Ntilde, hd1, t.e, t.M, t.a, t.u, t.w, t.z, t.nrows, t.cost);
     }
     {
         LaunchScope ls(P, KC_PLAN);
@@ -428,7 +454,7 @@ dvm_status_t build_table(dvm_plan_s *P)
 void free_table(dvm_plan_s *P)
 {
     DirTable &t = P->t;
-    void *ptrs[] = {t.e, t.M, t.a, t.u, t.w, t.nrows, t.row_off, t.cost, t.row_b, t.row_lo, t.row_hi,
+    void *ptrs[] = {t.e, t.M, t.a, t.u, t.w, t.z, t.nrows, t.row_off, t.cost, t.row_b, t.row_lo, t.row_hi,
                     t.off_in, t.off_out, t.local};
     for (void *q : ptrs)
         if (q) cudaFree(q);

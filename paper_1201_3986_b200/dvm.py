@@ -77,6 +77,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "dvm_profile_enable": ([P, ctypes.c_int], ctypes.c_int),
         "dvm_profile_read": ([P, V, V, ctypes.c_int], ctypes.c_int),
         "dvm_profile_name": ([ctypes.c_int], ctypes.c_char_p),
+        "dvm_set_path": ([P, ctypes.c_int], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -223,6 +224,10 @@ class Plan:
         _check(lib.dvm_euler(self._h, _dptr(f), float(dt), int(nsteps),
                              mom.ctypes.data if mom is not None else None), "dvm_euler")
         return mom
+
+    def set_path(self, path: int):
+        """0 = default kernels, 1 = v1 orbit sweeps (cross-check path)."""
+        _check(load().dvm_set_path(self._h, int(path)), "dvm_set_path")
 
     def profile(self, enable: bool = True):
         """Start (clear) / stop per-kernel CUDA-event timing inside libdvm."""

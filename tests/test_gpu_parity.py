@@ -279,3 +279,20 @@ def test_batched_edge_cases():
     torch.cuda.synchronize()
     o = out.cpu().numpy()
     assert np.array_equal(o[:, :256], Qb) and np.all(o[:, 256:] == 7.0)
+
+
+@pytest.mark.parametrize("d,N,Nbar,Nt,cells", [(3, 32, 4, 7, 1), (3, 64, 8, 14, 3), (3, 32, 3, 5, 40),
+                                               (3, 128, 2, 5, 1), (3, 64, 1, 4, 2)])
+def test_cluster_path_matches_orbit_path(d, N, Nbar, Nt, cells):
+    """The v2 cluster-per-cell kernel and the v1 orbit sweeps evaluate the same
+    operator (different summation orders): agreement to rounding."""
+    f = np.random.default_rng(N + cells).uniform(0.0, 1.0, size=(cells, N ** d))
+    p = _plan(d, N, Nbar, Ntilde=Nt)
+    q2 = _gpu(p, f)
+    p.set_path(1)
+    q1 = _gpu(p, f)
+    np.testing.assert_allclose(q2, q1, rtol=0, atol=1e-13 * np.abs(q1).max())
+    if N <= 64:
+        pts = np.arange(0, N ** d, N ** d // 97)
+        Qo, _, _ = oracle.collide(f[0], d, N, Nbar, Nt, 8.0, points=pts)
+        _assert_parity(q2[0][pts], Qo[0], f"cluster path N={N}", ref=np.abs(q1[0]).max())
