@@ -26,6 +26,9 @@
 // chunks with partial Q buffers reduced afterwards in chunk order.
 #include <cooperative_groups.h>
 
+#include <stdio.h>
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "dvm_internal.h"
@@ -190,9 +193,8 @@ __global__ void __launch_bounds__(kCT, 1) k_cluster3d(C3Args A)
             cluster.sync();
 
             // ---------------- phase B: e-orbit sweeps -> S, U, Q
-            {
-                const int gt = rank * kCT + threadIdx.x;
-                if (gt < NN * A.nseg) {
+            for (int gt = rank * kCT + threadIdx.x; gt < NN * A.nseg; gt += CL * kCT) {
+                {
                     const int r = gt % NN, seg = gt / NN;
                     // transversal axis: first non-fastest odd component of e
                     const int ja = (e0 & 1) ? 0 : ((e1 & 1) ? 1 : 2);
@@ -246,8 +248,11 @@ dvm_status_t launch(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q,
     DVM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     // cluster size: the one keeping the most SMs busy (ties: larger clusters,
     // fewer cells in flight, smaller L2 working set)
-    int best_cl = 0, best_nc = 0;
-    for (int cl : {16, 8, 4, 2}) {
+    int ncl[5] = {0, 0, 0, 0, 0};
+    const int cls[5] = {16, 8, 4, 2, 1};
+    int max_ctas = 0;
+    for (int ci = 0; ci < 5; ++ci) {
+        const int cl = cls[ci];
         cudaLaunchConfig_t cfg = {};
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -262,13 +267,23 @@ dvm_status_t launch(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q,
         int nc = 0;
         if (cudaOccupancyMaxActiveClusters(&nc, (void *)kern, &cfg) != cudaSuccess) {
             cudaGetLastError();
-            continue;
+            nc = 0;
         }
-        if (nc * cl > best_nc * best_cl) {
-            best_cl = cl;
-            best_nc = nc;
-        }
+        ncl[ci] = nc;
+        max_ctas = std::max(max_ctas, nc * cl);
     }
+    // largest cluster that still keeps >= 90% of the co-resident CTAs: one cell
+    // per cluster, so larger clusters mean fewer cells (f, T, Q) in flight in L2
+    int best_cl = 0, best_nc = 0;
+    for (int ci = 0; ci < 5; ++ci)
+        if (ncl[ci] > 0 && 10 * ncl[ci] * cls[ci] >= 9 * max_ctas) {
+            best_cl = cls[ci];
+            best_nc = ncl[ci];
+            break;
+        }
+    if (getenv("DVM_VERBOSE"))
+        fprintf(stderr, "[dvm] cluster3d N=%d: cluster=%d active_clusters=%d (max co-resident CTAs %d)\n", N,
+                best_cl, best_nc, max_ctas);
     if (best_cl == 0) {
         *handled = false;
         return DVM_OK;
