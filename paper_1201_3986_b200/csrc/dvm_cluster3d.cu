@@ -38,7 +38,6 @@ namespace cg = cooperative_groups;
 namespace dvm {
 namespace {
 
-constexpr int kCT = 1024;      // threads per CTA
 constexpr int kMaxRows = 256;  // perp-polygon rows held in shared memory
 
 struct C3Args {
@@ -65,12 +64,21 @@ __device__ __forceinline__ uint32_t pack3(int c0, int c1, int c2, int p)
     return ((uint32_t)(c0 & (N - 1)) << (2 * p)) | ((uint32_t)(c1 & (N - 1)) << p) | (uint32_t)(c2 & (N - 1));
 }
 
+// threads per CTA: 512 (two CTAs per SM) up to N = 64, 1024 for N = 128
 template <int N>
-__global__ void __launch_bounds__(kCT, 1) k_cluster3d(C3Args A)
+__host__ __device__ constexpr int cta_threads()
 {
-    constexpr int LPL = N / 32;   // row elements per lane in the prefix scan
-    constexpr int OUT = N / 32;   // outputs per thread per axis in phase A
+    return N >= 128 ? 1024 : 512;
+}
+
+template <int N>
+__global__ void __launch_bounds__(cta_threads<N>()) k_cluster3d(C3Args A)
+{
+    constexpr int kCT = cta_threads<N>();
     constexpr int NW = kCT / 32;  // warps per CTA
+    constexpr int LPL = N / 32;   // row elements per lane in the prefix scan
+    constexpr int OA = N / 32;    // outputs per thread along α (lane + 32 h)
+    constexpr int OB = N / NW;    // outputs per thread along β (warp + NW g)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double *sP = reinterpret_cast<double *>(smem_raw);  // [N][N] row prefix sums
     double *sTot = sP + N * N;                          // [N] row totals
@@ -155,20 +163,20 @@ __global__ void __launch_bounds__(kCT, 1) k_cluster3d(C3Args A)
                     if (lane == 31) sTot[beta] = x;
                 }
                 __syncthreads();
-                double t[OUT][OUT];
+                double t[OB][OA];
 #pragma unroll
-                for (int gg = 0; gg < OUT; ++gg)
+                for (int gg = 0; gg < OB; ++gg)
 #pragma unroll
-                    for (int h = 0; h < OUT; ++h) t[gg][h] = 0.0;
+                    for (int h = 0; h < OA; ++h) t[gg][h] = 0.0;
                 for (int k = 0; k < nr; ++k) {
                     const int b = sB[k], lo = sLo[k] - 1, hi = sHi[k];
 #pragma unroll
-                    for (int gg = 0; gg < OUT; ++gg) {
+                    for (int gg = 0; gg < OB; ++gg) {
                         const int rr = (warp + NW * gg + b) & (N - 1);
                         const double *row = sP + rr * N;
                         const double tot = sTot[rr];
 #pragma unroll
-                        for (int h = 0; h < OUT; ++h) {
+                        for (int h = 0; h < OA; ++h) {
                             const int al = lane + 32 * h;
                             const int ah = al + hi, aL = al + lo;
                             double s = row[ah & (N - 1)] - row[aL & (N - 1)];
@@ -179,11 +187,11 @@ __global__ void __launch_bounds__(kCT, 1) k_cluster3d(C3Args A)
                     }
                 }
 #pragma unroll
-                for (int gg = 0; gg < OUT; ++gg) {
+                for (int gg = 0; gg < OB; ++gg) {
                     const int beta = warp + NW * gg;
                     const int b0 = g * z0 + beta * w0, b1 = g * z1 + beta * w1, b2 = g * z2 + beta * w2;
 #pragma unroll
-                    for (int h = 0; h < OUT; ++h) {
+                    for (int h = 0; h < OA; ++h) {
                         const int al = lane + 32 * h;
                         Tb[pack3<N>(b0 + al * u0, b1 + al * u1, b2 + al * u2, p)] = t[gg][h];
                     }
@@ -243,6 +251,7 @@ dvm_status_t launch(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q,
                     int64_t ncells, bool *handled)
 {
     auto kern = k_cluster3d<N>;
+    constexpr int kCT = cta_threads<N>();
     const size_t smem = smem_bytes<N>();
     DVM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     DVM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -272,15 +281,24 @@ dvm_status_t launch(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q,
         ncl[ci] = nc;
         max_ctas = std::max(max_ctas, nc * cl);
     }
-    // largest cluster that still keeps >= 90% of the co-resident CTAs: one cell
-    // per cluster, so larger clusters mean fewer cells (f, T, Q) in flight in L2
+    // One cell per cluster: choose the cluster size by co-resident CTAs, scaled
+    // down when the cells in flight (f + T + Q = 3 N^3 doubles each) would not
+    // fit in ~96 MB of L2.
     int best_cl = 0, best_nc = 0;
-    for (int ci = 0; ci < 5; ++ci)
-        if (ncl[ci] > 0 && 10 * ncl[ci] * cls[ci] >= 9 * max_ctas) {
+    double best_score = -1.0;
+    const double cell_bytes = 3.0 * 8.0 * (double)N * N * N;
+    for (int ci = 0; ci < 5; ++ci) {
+        if (ncl[ci] <= 0) continue;
+        const double ws = ncl[ci] * cell_bytes;
+        const double score = (double)ncl[ci] * cls[ci] * std::min(1.0, 96.0e6 / ws);
+        if (score > best_score * 1.02) {
+            best_score = score;
             best_cl = cls[ci];
             best_nc = ncl[ci];
-            break;
         }
+        if (getenv("DVM_VERBOSE"))
+            fprintf(stderr, "[dvm]   cluster %2d: %3d clusters, score %.1f\n", cls[ci], ncl[ci], score);
+    }
     if (getenv("DVM_VERBOSE"))
         fprintf(stderr, "[dvm] cluster3d N=%d: cluster=%d active_clusters=%d (max co-resident CTAs %d)\n", N,
                 best_cl, best_nc, max_ctas);
