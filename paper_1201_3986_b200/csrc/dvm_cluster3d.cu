@@ -72,7 +72,7 @@ __host__ __device__ constexpr int cta_threads()
 }
 
 template <int N>
-__global__ void __launch_bounds__(cta_threads<N>()) k_cluster3d(C3Args A)
+__global__ void __launch_bounds__(cta_threads<N>(), 1024 / cta_threads<N>()) k_cluster3d(C3Args A)
 {
     constexpr int kCT = cta_threads<N>();
     constexpr int NW = kCT / 32;  // warps per CTA
@@ -217,20 +217,25 @@ __global__ void __launch_bounds__(cta_threads<N>()) k_cluster3d(C3Args A)
                     const uint32_t Ev = pack3<N>(e0, e1, e2, p);
                     const uint32_t Pin = pack3<N>((M + 1) * e0, (M + 1) * e1, (M + 1) * e2, p);
                     const uint32_t Pout = pack3<N>(-M * e0, -M * e1, -M * e2, p);
+                    const double *__restrict__ fr = fc;
+                    const double *__restrict__ Tr = Tb;
+                    double *__restrict__ Qr = Qc;
                     double Wf = 0.0, WT = 0.0;
                     uint32_t y = swar_add(x, Pout, H);
                     for (int m = -M; m <= M; ++m) {
-                        Wf += __ldg(fc + y);
-                        WT += Tb[y];
+                        Wf += __ldg(fr + y);
+                        WT += Tr[y];
                         y = swar_add(y, Ev, H);
                     }
+#pragma unroll 4
                     for (int s = 0; s < A.seg_len; ++s) {
-                        const double fx = __ldg(fc + x), Tx = Tb[x];
-                        const double S = Wf - fx, Uu = WT - Tx;
-                        Qc[x] += aw * (S * Tx - fx * Uu);
                         const uint32_t yi = swar_add(x, Pin, H), yo = swar_add(x, Pout, H);
-                        Wf += __ldg(fc + yi) - __ldg(fc + yo);
-                        WT += Tb[yi] - Tb[yo];
+                        const double fx = __ldg(fr + x), Tx = Tr[x];
+                        const double fi = __ldg(fr + yi), fo = __ldg(fr + yo), ti = Tr[yi], to = Tr[yo];
+                        const double S = Wf - fx, Uu = WT - Tx;
+                        Qr[x] += aw * (S * Tx - fx * Uu);
+                        Wf += fi - fo;
+                        WT += ti - to;
                         x = swar_add(x, Ev, H);
                     }
                 }
