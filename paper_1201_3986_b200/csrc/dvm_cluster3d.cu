@@ -71,20 +71,28 @@ __host__ __device__ constexpr int cta_threads()
     return N >= 128 ? 1024 : 512;
 }
 
+// Each shared-memory row holds the prefix sums extended periodically by HALO
+// nodes on both sides (P(k) = P(k mod N) + floor(k/N) * rowtotal), so the
+// window lookups of the perp-polygon rows never wrap.
+template <int N>
+__host__ __device__ constexpr int halo()
+{
+    return N >= 128 ? 32 : N / 2;
+}
+
 template <int N>
 __global__ void __launch_bounds__(cta_threads<N>(), 1024 / cta_threads<N>()) k_cluster3d(C3Args A)
 {
+    constexpr int HALO = halo<N>();
+    constexpr int STRIDE = N + 2 * HALO;
     constexpr int kCT = cta_threads<N>();
     constexpr int NW = kCT / 32;  // warps per CTA
     constexpr int LPL = N / 32;   // row elements per lane in the prefix scan
     constexpr int OA = N / 32;    // outputs per thread along α (lane + 32 h)
     constexpr int OB = N / NW;    // outputs per thread along β (warp + NW g)
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    double *sP = reinterpret_cast<double *>(smem_raw);  // [N][N] row prefix sums
-    double *sTot = sP + N * N;                          // [N] row totals
-    int *sB = reinterpret_cast<int *>(sTot + N);
-    int *sLo = sB + kMaxRows;
-    int *sHi = sLo + kMaxRows;
+    double *sP = reinterpret_cast<double *>(smem_raw);  // [N][STRIDE] extended row prefix sums
+    int4 *sRow = reinterpret_cast<int4 *>(sP + N * STRIDE);  // {b, lo-1, hi, 0} per polygon row
     __shared__ int s_meta[16];
 
     cg::cluster_group cluster = cg::this_cluster();
@@ -123,11 +131,8 @@ __global__ void __launch_bounds__(cta_threads<N>(), 1024 / cta_threads<N>()) k_c
             }
             __syncthreads();
             const int r0 = s_meta[13], nr = s_meta[14];
-            for (int k = threadIdx.x; k < nr; k += kCT) {
-                sB[k] = A.row_b[r0 + k];
-                sLo[k] = A.row_lo[r0 + k];
-                sHi[k] = A.row_hi[r0 + k];
-            }
+            for (int k = threadIdx.x; k < nr; k += kCT)
+                sRow[k] = make_int4(A.row_b[r0 + k], A.row_lo[r0 + k] - 1, A.row_hi[r0 + k], 0);
             const int e0 = s_meta[0], e1 = s_meta[1], e2 = s_meta[2];
             const int u0 = s_meta[3], u1 = s_meta[4], u2 = s_meta[5];
             const int w0 = s_meta[6], w1 = s_meta[7], w2 = s_meta[8];
@@ -158,31 +163,33 @@ __global__ void __launch_bounds__(cta_threads<N>(), 1024 / cta_threads<N>()) k_c
                         if (lane >= o) x += y;
                     }
                     const double excl = x - v[LPL - 1];
+                    const double rtot = __shfl_sync(0xffffffffu, x, 31);
+                    double *rowp = sP + beta * STRIDE + HALO;
 #pragma unroll
-                    for (int j = 0; j < LPL; ++j) sP[beta * N + lane * LPL + j] = v[j] + excl;
-                    if (lane == 31) sTot[beta] = x;
+                    for (int j = 0; j < LPL; ++j) {
+                        const int al = lane * LPL + j;
+                        const double pv = v[j] + excl;
+                        rowp[al] = pv;
+                        if (al >= N - HALO) rowp[al - N] = pv - rtot;
+                        if (al < HALO) rowp[al + N] = pv + rtot;
+                    }
                 }
                 __syncthreads();
-                double t[OB][OA];
+                double th[OB][OA], tl[OB][OA];
 #pragma unroll
                 for (int gg = 0; gg < OB; ++gg)
 #pragma unroll
-                    for (int h = 0; h < OA; ++h) t[gg][h] = 0.0;
+                    for (int h = 0; h < OA; ++h) th[gg][h] = tl[gg][h] = 0.0;
                 for (int k = 0; k < nr; ++k) {
-                    const int b = sB[k], lo = sLo[k] - 1, hi = sHi[k];
+                    const int4 rw = sRow[k];
 #pragma unroll
                     for (int gg = 0; gg < OB; ++gg) {
-                        const int rr = (warp + NW * gg + b) & (N - 1);
-                        const double *row = sP + rr * N;
-                        const double tot = sTot[rr];
+                        const double *rowp = sP + ((warp + NW * gg + rw.x) & (N - 1)) * STRIDE + HALO + lane;
+                        const double *ph = rowp + rw.z, *pl = rowp + rw.y;
 #pragma unroll
                         for (int h = 0; h < OA; ++h) {
-                            const int al = lane + 32 * h;
-                            const int ah = al + hi, aL = al + lo;
-                            double s = row[ah & (N - 1)] - row[aL & (N - 1)];
-                            const int wrap = (ah >> p) - (aL >> p);
-                            if (wrap) s += (double)wrap * tot;
-                            t[gg][h] += s;
+                            th[gg][h] += ph[32 * h];
+                            tl[gg][h] += pl[32 * h];
                         }
                     }
                 }
@@ -193,7 +200,7 @@ __global__ void __launch_bounds__(cta_threads<N>(), 1024 / cta_threads<N>()) k_c
 #pragma unroll
                     for (int h = 0; h < OA; ++h) {
                         const int al = lane + 32 * h;
-                        Tb[pack3<N>(b0 + al * u0, b1 + al * u1, b2 + al * u2, p)] = t[gg][h];
+                        Tb[pack3<N>(b0 + al * u0, b1 + al * u1, b2 + al * u2, p)] = th[gg][h] - tl[gg][h];
                     }
                 }
                 __syncthreads();
@@ -248,7 +255,7 @@ __global__ void __launch_bounds__(cta_threads<N>(), 1024 / cta_threads<N>()) k_c
 template <int N>
 size_t smem_bytes()
 {
-    return sizeof(double) * ((size_t)N * N + N) + sizeof(int) * 3 * kMaxRows;
+    return sizeof(double) * (size_t)N * (N + 2 * halo<N>()) + sizeof(int4) * kMaxRows;
 }
 
 template <int N>
@@ -403,6 +410,8 @@ dvm_status_t collide_cluster3d(dvm_plan_s *P, const double *f, int64_t f_stride,
     if (P->d != 3 || ncells <= 0 || P->local.empty()) return DVM_OK;
     for (int i : P->local)
         if (P->h_nrows[i] > kMaxRows) return DVM_OK;
+    const int hl = P->N >= 128 ? 32 : P->N / 2;
+    if (P->h_row_extent < 0 || P->h_row_extent > hl) return DVM_OK;
     switch (P->N) {
     case 32: return launch<32>(P, f, f_stride, Q, q_stride, ncells, handled);
     case 64: return launch<64>(P, f, f_stride, Q, q_stride, ncells, handled);
