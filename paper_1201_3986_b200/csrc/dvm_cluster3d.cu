@@ -56,6 +56,7 @@ struct C3Args {
     uint32_t H;
     int p;
     int seg_len, nseg;
+    int dbg;  // timing experiments only (DVM_C3_DEBUG): bit0 skip phase A, bit1 skip phase B
 };
 
 template <int N>
@@ -142,7 +143,7 @@ __global__ void __launch_bounds__(cta_threads<N>(), 1024 / cta_threads<N>()) k_c
             __syncthreads();
 
             // ---------------- phase A: T on this CTA's planes
-            for (int g = rank; g < N; g += CL) {
+            for (int g = rank; g < N && !(A.dbg & 1); g += CL) {
                 // row prefix sums of f on plane g (warp per row)
 #pragma unroll
                 for (int i = 0; i < N / NW; ++i) {
@@ -208,7 +209,7 @@ __global__ void __launch_bounds__(cta_threads<N>(), 1024 / cta_threads<N>()) k_c
             cluster.sync();
 
             // ---------------- phase B: e-orbit sweeps -> S, U, Q
-            for (int gt = rank * kCT + threadIdx.x; gt < NN * A.nseg; gt += CL * kCT) {
+            for (int gt = rank * kCT + threadIdx.x; gt < NN * A.nseg && !(A.dbg & 2); gt += CL * kCT) {
                 {
                     const int r = gt % NN, seg = gt / NN;
                     // transversal axis: first non-fastest odd component of e
@@ -367,6 +368,7 @@ dvm_status_t launch(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q,
     while (nseg * 2 <= best_cl * kCT / (N * N) && N / (nseg * 2) >= 8) nseg *= 2;
     a.nseg = nseg;
     a.seg_len = N / nseg;
+    a.dbg = getenv("DVM_C3_DEBUG") ? atoi(getenv("DVM_C3_DEBUG")) : 0;
     // zero the accumulation target
     if (nchunks == 1) {
         dvm_status_t st = zero_cells(P, Q, q_stride, ncells, nodes);
