@@ -69,9 +69,10 @@ struct Workspace {
     double *mom_dev = nullptr;      // [(steps+1)][kMaxD+2]
     size_t mom_rows = 0;
     double *qtmp = nullptr;         // euler scratch (nodes)
-    double *c3_T = nullptr;         // v2 cluster kernel: per-cluster T buffers
-    double *c3_part = nullptr;      // v2 cluster kernel: per-chunk partial Q
-    size_t c3_T_elems = 0, c3_part_elems = 0;
+    double2 *c3_f = nullptr;        // cluster kernel: interleaved cell pairs of f
+    double2 *c3_q = nullptr;        // cluster kernel: interleaved partial Q per direction chunk
+    double2 *c3_t = nullptr;        // cluster kernel: per-cluster T buffers
+    size_t c3_f_elems = 0, c3_q_elems = 0, c3_t_elems = 0;
 };
 
 }  // namespace dvm

@@ -282,7 +282,7 @@ def test_batched_edge_cases():
 
 
 @pytest.mark.parametrize("d,N,Nbar,Nt,cells", [(3, 32, 4, 7, 1), (3, 64, 8, 14, 3), (3, 32, 3, 5, 40),
-                                               (3, 128, 2, 5, 1), (3, 64, 1, 4, 2)])
+                                               (3, 64, 2, 5, 1), (3, 64, 1, 4, 2), (3, 32, 4, 7, 3)])
 def test_cluster_path_matches_orbit_path(d, N, Nbar, Nt, cells):
     """The v2 cluster-per-cell kernel and the v1 orbit sweeps evaluate the same
     operator (different summation orders): agreement to rounding."""
