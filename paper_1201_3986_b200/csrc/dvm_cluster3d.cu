@@ -335,6 +335,14 @@ dvm_status_t launch(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q,
             best_nc = ncl[ci];
         }
     }
+    if (getenv("DVM_C3_CLUSTER")) {  // experiment override
+        const int want = atoi(getenv("DVM_C3_CLUSTER"));
+        for (int ci = 0; ci < 5; ++ci)
+            if (cls[ci] == want && ncl[ci] > 0) {
+                best_cl = want;
+                best_nc = ncl[ci];
+            }
+    }
     if (best_cl == 0) return DVM_OK;  // not launchable: caller uses the orbit kernels
     if (getenv("DVM_VERBOSE"))
         fprintf(stderr, "[dvm] cluster3d N=%d: cluster=%d active_clusters=%d\n", N, best_cl, best_nc);
