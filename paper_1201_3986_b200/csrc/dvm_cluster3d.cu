@@ -21,10 +21,11 @@
 //            then T(α, β) = Σ_b [P(β+b, α+hi_b) − P(β+b, α+lo_b−1)] and
 //            stores T to the cluster's L2-resident T buffer.
 //   cluster barrier (release/acquire: T visible to the whole cluster)
-//   phase B  node-owned stencil in storage order (every access coalesced,
-//            each thread owns the same nodes for all directions):
-//            S = Σ_{1<=|m|<=M} f(x+me), U = Σ_{1<=|m|<=M} T(x+me),
+//   phase B  S = Σ_{1<=|m|<=M} f(x+me), U = Σ_{1<=|m|<=M} T(x+me),
 //            Q(x) += a_e (S T(x) − f(x) U)      (eq:decD)
+//            by sliding windows along segments of e-orbits (lanes on adjacent
+//            orbits, coalesced when e_0 or e_1 is odd), else by a node-owned
+//            stencil in storage order (always coalesced).
 //   cluster barrier
 // Q accumulates in direction order: bitwise deterministic, no atomics.  One
 // pair of cells per cluster keeps f + T + Q of the cells in flight in L2.
@@ -90,6 +91,7 @@ __global__ void __launch_bounds__(kCT, 1) k_cluster3d(C3Args A)
     constexpr int OA = N / 32;   // outputs along α per thread (lane + 32 h)
     constexpr int OB = N / NW;   // outputs along β per thread (warp + NW g)
     constexpr int64_t NODES = (int64_t)N * N * N;
+    constexpr int NN = N * N;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double2 *sP = reinterpret_cast<double2 *>(smem_raw);      // [N][STRIDE]
     int4 *sRow = reinterpret_cast<int4 *>(sP + N * STRIDE);   // {b, lo-1, hi, 0}
@@ -207,24 +209,65 @@ __global__ void __launch_bounds__(kCT, 1) k_cluster3d(C3Args A)
             }
             cluster.sync();
 
-            // ---------------- phase B: node-owned stencil along e (coalesced)
+            // ---------------- phase B: S, U along e and the Q update
             if (!(A.dbg & 2)) {
                 const double2 *__restrict__ Tr = Tb;
-                for (int64_t x = (int64_t)rank * kCT + threadIdx.x; x < NODES; x += (int64_t)CL * kCT) {
-                    const uint32_t xi = (uint32_t)x;
-                    const double2 f0 = __ldg(fc + xi), T0 = Tr[xi];
-                    double2 S = make_double2(0.0, 0.0), Uu = make_double2(0.0, 0.0);
-                    for (int m = 1; m <= M; ++m) {
-                        const uint2 o = sOff[m];
-                        const uint32_t xp = swar_add(xi, o.x, H), xm = swar_add(xi, o.y, H);
-                        const double2 fp = __ldg(fc + xp), fm = __ldg(fc + xm), tp = Tr[xp], tm = Tr[xm];
-                        S = add2(S, add2(fp, fm));
-                        Uu = add2(Uu, add2(tp, tm));
+                if ((e0 & 1) || (e1 & 1)) {
+                    // e-orbit segments of length N/SEGS, one per thread: lanes walk
+                    // adjacent orbits (consecutive fastest-axis nodes: coalesced) and
+                    // slide the windows in registers (enter/leave per step).
+                    constexpr int SEGS = (16 * kCT) / NN < N / 8 ? ((16 * kCT) / NN > 0 ? (16 * kCT) / NN : 1) : N / 8;
+                    constexpr int SL = N / SEGS;
+                    const int ja = (e0 & 1) ? 0 : 1;
+                    const uint32_t Ev = sOff[1].x;
+                    const uint32_t Pin = pack3<N>((M + 1) * e0, (M + 1) * e1, (M + 1) * e2, p);
+                    const uint32_t Pout = sOff[M].y;
+                    for (int gt = rank * kCT + threadIdx.x; gt < NN * SEGS; gt += CL * kCT) {
+                        const int r = gt % NN, seg = gt / NN;
+                        const int hiF = r >> p, loF = r & (N - 1);
+                        const int c0 = ja == 0 ? 0 : hiF, c1 = ja == 0 ? hiF : 0;
+                        const int t0 = seg * SL;
+                        uint32_t x = pack3<N>(c0 + t0 * e0, c1 + t0 * e1, loF + t0 * e2, p);
+                        double2 Wf = make_double2(0.0, 0.0), WT = make_double2(0.0, 0.0);
+                        uint32_t y = swar_add(x, Pout, H);
+                        for (int m = -M; m <= M; ++m) {
+                            Wf = add2(Wf, __ldg(fc + y));
+                            WT = add2(WT, Tr[y]);
+                            y = swar_add(y, Ev, H);
+                        }
+#pragma unroll 4
+                        for (int s = 0; s < SL; ++s) {
+                            const uint32_t yi = swar_add(x, Pin, H), yo = swar_add(x, Pout, H);
+                            const double2 f0 = __ldg(fc + x), T0 = Tr[x];
+                            const double2 fi = __ldg(fc + yi), fo = __ldg(fc + yo), ti = Tr[yi], to = Tr[yo];
+                            const double2 S = sub2(Wf, f0), Uu = sub2(WT, T0);
+                            double2 q = Qc[x];
+                            q.x += aw * (S.x * T0.x - f0.x * Uu.x);
+                            q.y += aw * (S.y * T0.y - f0.y * Uu.y);
+                            Qc[x] = q;
+                            Wf = add2(Wf, sub2(fi, fo));
+                            WT = add2(WT, sub2(ti, to));
+                            x = swar_add(x, Ev, H);
+                        }
                     }
-                    double2 q = Qc[xi];
-                    q.x += aw * (S.x * T0.x - f0.x * Uu.x);
-                    q.y += aw * (S.y * T0.y - f0.y * Uu.y);
-                    Qc[xi] = q;
+                } else {
+                    // e0, e1 even: node-owned stencil in storage order (coalesced)
+                    for (int64_t x = (int64_t)rank * kCT + threadIdx.x; x < NODES; x += (int64_t)CL * kCT) {
+                        const uint32_t xi = (uint32_t)x;
+                        const double2 f0 = __ldg(fc + xi), T0 = Tr[xi];
+                        double2 S = make_double2(0.0, 0.0), Uu = make_double2(0.0, 0.0);
+                        for (int m = 1; m <= M; ++m) {
+                            const uint2 o = sOff[m];
+                            const uint32_t xp = swar_add(xi, o.x, H), xm = swar_add(xi, o.y, H);
+                            const double2 fp = __ldg(fc + xp), fm = __ldg(fc + xm), tp = Tr[xp], tm = Tr[xm];
+                            S = add2(S, add2(fp, fm));
+                            Uu = add2(Uu, add2(tp, tm));
+                        }
+                        double2 q = Qc[xi];
+                        q.x += aw * (S.x * T0.x - f0.x * Uu.x);
+                        q.y += aw * (S.y * T0.y - f0.y * Uu.y);
+                        Qc[xi] = q;
+                    }
                 }
             }
             cluster.sync();

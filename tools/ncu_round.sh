@@ -4,7 +4,7 @@
 set -x
 TAG=${1:-r01}
 KREG=${2:-k_rowsum}
-CMD="python bench.py --cells 16 --steps 1 --warmup 3 --no-cpu-baseline"
+CMD="python bench.py --cells ${CELLS:-14} --steps 1 --warmup 3 --no-cpu-baseline"
 mkdir -p gpurun_out
 $CMD > gpurun_out/plain_${TAG}.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv \
