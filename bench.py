@@ -229,10 +229,14 @@ def run_ours(args):
     top = max(prof.items(), key=lambda kv: kv[1][0])
     top_name, (top_ms, top_n) = top
     # algorithmic bytes per launch of the dominant kernel: the streaming
-    # formulation charges 8 N^3 bytes per (cell, direction);
-    # one k_rowsum launch processes one direction for all cells of the batch.
-    per_launch_units = cells * (plan.info()["A_local"] / max(1, prof["k_rowsum"][1] / psteps))
-    alg_bytes = 8.0 * nodes * per_launch_units
+    # formulation charges (A+2)*8*N^3 bytes per cell-evaluation
+    # (one f pass per direction + f read + Q write).  k_cluster3d evaluates the
+    # whole batch (all cells, all directions) in one launch; the v1 orbit path
+    # launches k_rowsum once per direction chunk.
+    if top_name == "k_cluster3d":
+        alg_bytes = (A + 2) * 8.0 * nodes * cells * psteps / top_n
+    else:
+        alg_bytes = (A + 2) * 8.0 * nodes * cells * psteps / max(1, prof.get("k_rowsum", (0, 1))[1])
     avg_launch_s = top_ms / top_n / 1e3
     peak, peak_src = _peaks()
     achieved = alg_bytes / avg_launch_s / 1e9
