@@ -69,7 +69,30 @@ struct C3Args {
     uint32_t H;
     int p;
     int dbg;  // timing experiments only (DVM_C3_DEBUG): bit0 skip phase A, bit1 skip phase B
+    int gsize;            // software groups: CTAs per group (SOFT kernels)
+    unsigned int *gctr;   // software groups: one barrier counter per group
 };
+
+// Group barrier for SOFT (cooperative-launch) kernels: every CTA of the group
+// arrives on a monotonic counter; thread 0 publishes the CTA's writes with a
+// gpu-scope fence, then acquire-polls until all gsize CTAs of this epoch
+// arrived (the acquire also invalidates the SM's L1, so later plain loads see
+// the other CTAs' T and Q).
+__device__ __forceinline__ void group_barrier(unsigned int *ctr, unsigned int target)
+{
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(ctr, 1u);
+        unsigned int v;
+        for (;;) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+            if (v >= target) break;
+            __nanosleep(32);
+        }
+    }
+    __syncthreads();
+}
 
 template <int N>
 __device__ __forceinline__ uint32_t pack3(int c0, int c1, int c2, int p)
@@ -80,7 +103,7 @@ __device__ __forceinline__ uint32_t pack3(int c0, int c1, int c2, int p)
 __device__ __forceinline__ double2 add2(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 sub2(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
 
-template <int N>
+template <int N, bool SOFT>
 __global__ void __launch_bounds__(kCT, 1) k_cluster3d(C3Args A)
 {
     constexpr int HALO = halo<N>();
@@ -98,11 +121,19 @@ __global__ void __launch_bounds__(kCT, 1) k_cluster3d(C3Args A)
     uint2 *sOff = reinterpret_cast<uint2 *>(sRow + kMaxRows);  // {pack(m e), pack(-m e)}, m = 1..M
     __shared__ int s_meta[16];
 
-    cg::cluster_group cluster = cg::this_cluster();
-    const int CL = (int)cluster.num_blocks();
-    const int rank = (int)cluster.block_rank();
+    const int CL = SOFT ? A.gsize : (int)cg::this_cluster().num_blocks();
+    const int rank = SOFT ? (int)(blockIdx.x % CL) : (int)cg::this_cluster().block_rank();
     const int cid = blockIdx.x / CL;
     const int nclusters = gridDim.x / CL;
+    unsigned int epoch = 0;
+    auto barrier = [&]() {
+        if constexpr (SOFT) {
+            ++epoch;
+            group_barrier(A.gctr + cid, epoch * (unsigned)CL);
+        } else {
+            cg::this_cluster().sync();
+        }
+    };
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int p = A.p;
     const uint32_t H = A.H;
@@ -207,7 +238,7 @@ __global__ void __launch_bounds__(kCT, 1) k_cluster3d(C3Args A)
                 }
                 __syncthreads();
             }
-            cluster.sync();
+            barrier();
 
             // ---------------- phase B: S, U along e and the Q update
             if (!(A.dbg & 2)) {
@@ -270,7 +301,7 @@ __global__ void __launch_bounds__(kCT, 1) k_cluster3d(C3Args A)
                     }
                 }
             }
-            cluster.sync();
+            barrier();
         }
     }
 }
@@ -339,56 +370,78 @@ template <int N>
 dvm_status_t launch(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q, int64_t q_stride,
                     int64_t ncells, bool *handled)
 {
-    auto kern = k_cluster3d<N>;
+    auto kern = k_cluster3d<N, false>;
+    auto kern_soft = k_cluster3d<N, true>;
     const size_t smem = smem_bytes<N>();
     DVM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     DVM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    const int cls[5] = {16, 8, 4, 2, 1};
-    int ncl[5] = {0, 0, 0, 0, 0};
-    for (int ci = 0; ci < 5; ++ci) {
-        cudaLaunchConfig_t cfg = {};
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = cls[ci];
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.gridDim = dim3(cls[ci], 1, 1);
-        cfg.blockDim = dim3(kCT, 1, 1);
-        cfg.dynamicSmemBytes = smem;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        if (cudaOccupancyMaxActiveClusters(&ncl[ci], (void *)kern, &cfg) != cudaSuccess) {
-            cudaGetLastError();
-            ncl[ci] = 0;
-        }
-    }
-    // One pair of cells per cluster: score = SMs kept busy, scaled down when the
-    // pairs in flight (f + T + Q, 3 x 16 N^3 bytes each) exceed ~100 MB of L2.
+    DVM_CUDA(cudaFuncSetAttribute(kern_soft, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const bool verbose = getenv("DVM_VERBOSE") != nullptr;
+    // Mode "soft" (default): cooperative launch, software groups of 16 CTAs
+    // (one per SM) -- free of the GPC packing limits of hardware clusters.
+    // Mode "cluster": hardware thread-block clusters.
+    const char *mode_env = getenv("DVM_C3_MODE");
+    const bool soft = !(mode_env && mode_env[0] == 'c');
     int best_cl = 0, best_nc = 0;
-    double best_score = -1.0;
     const double pair_bytes = 3.0 * 16.0 * (double)N * N * N;
-    for (int ci = 0; ci < 5; ++ci) {
-        if (ncl[ci] <= 0) continue;
-        const double score = (double)ncl[ci] * cls[ci] * std::min(1.0, 100.0e6 / (ncl[ci] * pair_bytes));
-        if (getenv("DVM_VERBOSE"))
-            fprintf(stderr, "[dvm]   cluster %2d: %3d clusters, score %.1f\n", cls[ci], ncl[ci], score);
-        if (score > best_score * 1.02) {
-            best_score = score;
-            best_cl = cls[ci];
-            best_nc = ncl[ci];
+    if (soft) {
+        int dev = 0, sms = 0, per_sm = 0, coop = 0;
+        DVM_CUDA(cudaGetDevice(&dev));
+        DVM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        DVM_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+        DVM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern_soft, kCT, smem));
+        if (!coop || per_sm < 1) return DVM_OK;
+        best_cl = 16;
+        // groups in flight: all co-resident CTAs, capped by ~110 MB of L2 for
+        // the pairs in flight (f + T + Q each)
+        best_nc = std::min((sms * per_sm) / best_cl, std::max(1, (int)(110.0e6 / pair_bytes)));
+        if (getenv("DVM_C3_GROUPS")) best_nc = std::min(best_nc, std::max(1, atoi(getenv("DVM_C3_GROUPS"))));
+        if (verbose)
+            fprintf(stderr, "[dvm] cluster3d N=%d: soft groups of %d CTAs, %d groups (co-resident CTAs %d)\n", N,
+                    best_cl, best_nc, sms * per_sm);
+    } else {
+        const int cls[5] = {16, 8, 4, 2, 1};
+        int ncl[5] = {0, 0, 0, 0, 0};
+        for (int ci = 0; ci < 5; ++ci) {
+            cudaLaunchConfig_t cfg = {};
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = cls[ci];
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.gridDim = dim3(cls[ci], 1, 1);
+            cfg.blockDim = dim3(kCT, 1, 1);
+            cfg.dynamicSmemBytes = smem;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            if (cudaOccupancyMaxActiveClusters(&ncl[ci], (void *)kern, &cfg) != cudaSuccess) {
+                cudaGetLastError();
+                ncl[ci] = 0;
+            }
         }
-    }
-    if (getenv("DVM_C3_CLUSTER")) {  // experiment override
-        const int want = atoi(getenv("DVM_C3_CLUSTER"));
-        for (int ci = 0; ci < 5; ++ci)
-            if (cls[ci] == want && ncl[ci] > 0) {
-                best_cl = want;
+        // score = SMs kept busy, scaled down when the pairs in flight exceed ~100 MB of L2
+        double best_score = -1.0;
+        for (int ci = 0; ci < 5; ++ci) {
+            if (ncl[ci] <= 0) continue;
+            const double score = (double)ncl[ci] * cls[ci] * std::min(1.0, 100.0e6 / (ncl[ci] * pair_bytes));
+            if (verbose) fprintf(stderr, "[dvm]   cluster %2d: %3d clusters, score %.1f\n", cls[ci], ncl[ci], score);
+            if (score > best_score * 1.02) {
+                best_score = score;
+                best_cl = cls[ci];
                 best_nc = ncl[ci];
             }
+        }
+        if (getenv("DVM_C3_CLUSTER")) {  // experiment override
+            const int want = atoi(getenv("DVM_C3_CLUSTER"));
+            for (int ci = 0; ci < 5; ++ci)
+                if (cls[ci] == want && ncl[ci] > 0) {
+                    best_cl = want;
+                    best_nc = ncl[ci];
+                }
+        }
+        if (best_cl == 0) return DVM_OK;  // not launchable: caller uses the orbit kernels
+        if (verbose) fprintf(stderr, "[dvm] cluster3d N=%d: cluster=%d active_clusters=%d\n", N, best_cl, best_nc);
     }
-    if (best_cl == 0) return DVM_OK;  // not launchable: caller uses the orbit kernels
-    if (getenv("DVM_VERBOSE"))
-        fprintf(stderr, "[dvm] cluster3d N=%d: cluster=%d active_clusters=%d\n", N, best_cl, best_nc);
     const int nloc = (int)P->local.size();
     const int64_t nodes = (int64_t)N * N * N;
     const int64_t ngroups = (ncells + 1) / 2;
@@ -428,19 +481,29 @@ dvm_status_t launch(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q,
     a.H = P->pk.H;
     a.p = P->p;
     a.dbg = getenv("DVM_C3_DEBUG") ? atoi(getenv("DVM_C3_DEBUG")) : 0;
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = best_cl;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.gridDim = dim3(nclusters * best_cl, 1, 1);
-    cfg.blockDim = dim3(kCT, 1, 1);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = P->stream;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    {
+    a.gsize = best_cl;
+    a.gctr = nullptr;
+    if (soft) {
+        if ((st = grow(&w.c3_ctr, &w.c3_ctr_elems, (size_t)nclusters, P->stream))) return st;
+        DVM_CUDA(cudaMemsetAsync(w.c3_ctr, 0, sizeof(unsigned int) * nclusters, P->stream));
+        a.gctr = w.c3_ctr;
+        void *args[] = {&a};
+        LaunchScope ls(P, KC_CLUSTER3D);
+        DVM_CUDA(cudaLaunchCooperativeKernel((void *)kern_soft, dim3(nclusters * best_cl), dim3(kCT), args, smem,
+                                             P->stream));
+    } else {
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = best_cl;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(nclusters * best_cl, 1, 1);
+        cfg.blockDim = dim3(kCT, 1, 1);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = P->stream;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
         LaunchScope ls(P, KC_CLUSTER3D);
         DVM_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
     }

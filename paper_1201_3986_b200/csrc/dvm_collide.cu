@@ -412,7 +412,7 @@ void free_workspace(dvm_plan_s *P)
 {
     clear_profile(P);
     Workspace &w = P->ws;
-    void *ptrs[] = {w.S, w.part, w.f_stage, w.q_stage, w.mom_partial, w.mom_dev, w.qtmp, w.c3_f, w.c3_q, w.c3_t};
+    void *ptrs[] = {w.S, w.part, w.f_stage, w.q_stage, w.mom_partial, w.mom_dev, w.qtmp, w.c3_f, w.c3_q, w.c3_t, w.c3_ctr};
     for (void *q : ptrs)
         if (q) cudaFree(q);
     w = Workspace{};

@@ -72,7 +72,8 @@ struct Workspace {
     double2 *c3_f = nullptr;        // cluster kernel: interleaved cell pairs of f
     double2 *c3_q = nullptr;        // cluster kernel: interleaved partial Q per direction chunk
     double2 *c3_t = nullptr;        // cluster kernel: per-cluster T buffers
-    size_t c3_f_elems = 0, c3_q_elems = 0, c3_t_elems = 0;
+    unsigned int *c3_ctr = nullptr; // cluster kernel (soft groups): barrier counters
+    size_t c3_f_elems = 0, c3_q_elems = 0, c3_t_elems = 0, c3_ctr_elems = 0;
 };
 
 }  // namespace dvm
