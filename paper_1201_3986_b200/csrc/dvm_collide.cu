@@ -315,7 +315,7 @@ dvm_status_t collide_batched(dvm_plan_s *P, const double *f, double *Q, int64_t 
     if (ncells == 0) return DVM_OK;
     if (P->d == 3 && !P->force_v1) {
         bool handled = false;
-        dvm_status_t st = collide_cluster3d(P, f, stride, Q, stride, ncells, &handled);
+        dvm_status_t st = collide_gain3d(P, f, stride, Q, stride, ncells, &handled);
         if (st || handled) return st;
     }
     const int zero_blocks = 592;
@@ -412,7 +412,7 @@ void free_workspace(dvm_plan_s *P)
 {
     clear_profile(P);
     Workspace &w = P->ws;
-    void *ptrs[] = {w.S, w.part, w.f_stage, w.q_stage, w.mom_partial, w.mom_dev, w.qtmp, w.c3_f, w.c3_q, w.c3_t, w.c3_ctr};
+    void *ptrs[] = {w.S, w.part, w.f_stage, w.q_stage, w.mom_partial, w.mom_dev, w.qtmp, w.fft_z, w.g3_t, w.g3_q, w.g3_ctr};
     for (void *q : ptrs)
         if (q) cudaFree(q);
     w = Workspace{};

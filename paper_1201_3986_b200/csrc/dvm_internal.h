@@ -69,20 +69,33 @@ struct Workspace {
     double *mom_dev = nullptr;      // [(steps+1)][kMaxD+2]
     size_t mom_rows = 0;
     double *qtmp = nullptr;         // euler scratch (nodes)
-    double2 *c3_f = nullptr;        // cluster kernel: interleaved cell pairs of f
-    double2 *c3_q = nullptr;        // cluster kernel: interleaved partial Q per direction chunk
-    double2 *c3_t = nullptr;        // cluster kernel: per-cluster T buffers
-    unsigned int *c3_ctr = nullptr; // cluster kernel (soft groups): barrier counters
-    size_t c3_f_elems = 0, c3_q_elems = 0, c3_t_elems = 0, c3_ctr_elems = 0;
+    double2 *fft_z = nullptr;       // 3D loss: complex FFT workspace [pairs][nodes]
+    double *g3_t = nullptr;         // 3D gain: per-group ping-pong T_e buffers [groups][2][nodes]
+    double *g3_q = nullptr;         // 3D gain: per-chunk partial Q (small batches)
+    unsigned int *g3_ctr = nullptr; // 3D gain: group barrier counters
+    size_t fft_z_elems = 0, g3_t_elems = 0, g3_q_elems = 0, g3_ctr_elems = 0;
 };
 
 }  // namespace dvm
 
 namespace dvm {
-enum KernelClass { KC_LINESUM = 0, KC_ROWSUM, KC_REDUCE, KC_ZERO, KC_MOMENTS, KC_AXPY, KC_PLAN, KC_CLUSTER3D, KC_COUNT };
+enum KernelClass { KC_LINESUM = 0, KC_ROWSUM, KC_REDUCE, KC_ZERO, KC_MOMENTS, KC_AXPY, KC_PLAN, KC_GAIN3D, KC_FFT, KC_COUNT };
 struct ProfRec {
     int cls;
     cudaEvent_t a, b;
+};
+}  // namespace dvm
+
+namespace dvm {
+// Plan tables of the 3D gain/loss path (dvm_gain3d.cu, dvm_frame.h).
+struct GainTables {
+    bool ready = false;
+    int *meta = nullptr;      // [A_local][24] frame + program header per local direction
+    int4 *prog = nullptr;     // sliding-program entries (rho, t1, t2, sign)
+    double *aw = nullptr;     // [A_local] a_e
+    double2 *tw = nullptr;    // FFT twiddles exp(-2πik/N), k < N/2
+    double *lamhat = nullptr; // [N^3] spectrum of the loss kernel λ (real)
+    size_t bytes = 0;
 };
 }  // namespace dvm
 
@@ -101,6 +114,7 @@ struct dvm_plan_s {
     std::vector<int> local;      // direction indices evaluated by this plan, ascending
     std::vector<uint8_t> is_local;
     dvm::Workspace ws;
+    dvm::GainTables g;
     uint64_t launches = 0;
     size_t table_bytes = 0;
     bool profiling = false;
@@ -157,8 +171,10 @@ dvm_status_t axpy(dvm_plan_s *P, double *f, const double *q, double dt);
 dvm_status_t zero_cells(dvm_plan_s *P, double *Q, int64_t q_stride, int64_t ncells, int64_t nodes);
 dvm_status_t reduce_slots(dvm_plan_s *P, double *Q, int64_t q_stride, const double *part, int64_t slot_elems,
                           int nslots, int64_t ncells, int64_t nodes);
-dvm_status_t collide_cluster3d(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q, int64_t q_stride,
-                               int64_t ncells, bool *handled);
+dvm_status_t build_gain3d(dvm_plan_s *P);
+void free_gain3d(dvm_plan_s *P);
+dvm_status_t collide_gain3d(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q, int64_t q_stride,
+                            int64_t ncells, bool *handled);
 void free_workspace(dvm_plan_s *P);
 
 }  // namespace dvm

@@ -457,7 +457,8 @@ dvm_status_t build_table(dvm_plan_s *P)
         DVM_CUDA(cudaMemcpyAsync(t.local, P->local.data(), sizeof(int) * P->local.size(), cudaMemcpyHostToDevice,
                                  P->stream));
     DVM_CUDA(cudaStreamSynchronize(P->stream));
-    P->table_bytes = acc;
+    if ((st = build_gain3d(P))) return st;
+    P->table_bytes = acc + P->g.bytes;
     return DVM_OK;
 }
 
@@ -469,6 +470,7 @@ void free_table(dvm_plan_s *P)
     for (void *q : ptrs)
         if (q) cudaFree(q);
     t = DirTable{};
+    free_gain3d(P);
 }
 
 }  // namespace dvm

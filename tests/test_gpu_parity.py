@@ -214,7 +214,12 @@ def test_c2_euler_trajectory():
 def test_constant_field(d, N, Nbar):
     p = _plan(d, N, Nbar)
     Q1 = _gpu(p, np.ones(N ** d))
-    assert np.all(Q1 == 0.0)  # every sum is an exact small integer (reading R18)
+    if d == 2:
+        assert np.all(Q1 == 0.0)  # every sum is an exact small integer (reading R18)
+    else:
+        # the 3D loss is an FFT convolution: exact only up to rounding (reading R18)
+        _, G1, _ = oracle.collide(np.ones(N ** d), d, N, Nbar, p.Ntilde, 8.0, points=np.arange(4))
+        assert np.abs(Q1).max() <= 1e-13 * G1.max()
     Qc = _gpu(p, np.full(N ** d, 0.3))
     _, G, _ = oracle.collide(np.full(N ** d, 0.3), d, N, Nbar, p.Ntilde, 8.0, points=np.arange(4))
     assert np.abs(Qc).max() <= 1e-13 * G.max()

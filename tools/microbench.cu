@@ -58,6 +58,58 @@ __global__ void k_read(const double2 *in, size_t n, int reps, double *out)
     out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
 }
 
+template <typename T>
+__global__ void k_gather(const T *in, size_t mask, size_t stride, int reps, double *out)
+{
+    double acc = 0;
+    const size_t n = mask + 1;
+    for (int r = 0; r < reps; ++r)
+        for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+            T v = in[(i * stride + r) & mask];
+            acc += *reinterpret_cast<double *>(&v);
+        }
+    out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+template <typename T>
+__global__ void k_scatter(T *buf, size_t mask, size_t stride, int reps)
+{
+    const size_t n = mask + 1;
+    for (int r = 0; r < reps; ++r)
+        for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+            T v;
+            *reinterpret_cast<double *>(&v) = (double)i;
+            buf[(i * stride + r) & mask] = v;
+        }
+}
+template <typename T>
+double time_gather(const void *buf, size_t bytes, size_t stride, int sms, double *out)
+{
+    size_t n = bytes / sizeof(T);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a); cudaEventCreate(&b);
+    k_gather<T><<<sms * 8, 256>>>((const T *)buf, n - 1, stride, 2, out);
+    cudaEventRecord(a);
+    k_gather<T><<<sms * 8, 256>>>((const T *)buf, n - 1, stride, 20, out);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    return 20.0 * n * sizeof(T) / (ms * 1e-3);
+}
+template <typename T>
+double time_scatter(void *buf, size_t bytes, size_t stride, int sms)
+{
+    size_t n = bytes / sizeof(T);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a); cudaEventCreate(&b);
+    k_scatter<T><<<sms * 8, 256>>>((T *)buf, n - 1, stride, 2);
+    cudaEventRecord(a);
+    k_scatter<T><<<sms * 8, 256>>>((T *)buf, n - 1, stride, 20);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    return 20.0 * n * sizeof(T) / (ms * 1e-3);
+}
+
 int main()
 {
     int sms;
@@ -110,6 +162,17 @@ int main()
     CK(cudaEventSynchronize(b));
     cudaEventElapsedTime(&ms, a, b);
     double hbm = (double)nh * 16 / (ms * 1e-3);
+    // L2-resident gathers/scatters over 32 MB: stride 1 (coalesced) vs odd stride (one element per sector)
+    for (size_t st : {(size_t)1, (size_t)4099}) {
+        printf("{\"l2_32MB_stride\": %zu, \"gather8\": %.4e, \"gather16\": %.4e, \"gather32\": %.4e, \"scatter8\": %.4e, \"scatter16\": %.4e, \"scatter32\": %.4e}\n", st,
+               time_gather<double>(buf, 32u << 20, st, sms, out), time_gather<double2>(buf, 32u << 20, st, sms, out),
+               time_gather<double4>(buf, 32u << 20, st, sms, out), time_scatter<double>(buf, 32u << 20, st, sms),
+               time_scatter<double2>(buf, 32u << 20, st, sms), time_scatter<double4>(buf, 32u << 20, st, sms));
+    }
+    for (size_t mb : {(size_t)8, (size_t)64, (size_t)96}) {
+        printf("{\"l2_MB\": %zu, \"read16\": %.4e, \"gather16_odd\": %.4e}\n", mb,
+               time_gather<double2>(buf, mb << 20, 1, sms, out), time_gather<double2>(buf, mb << 20, 4099, sms, out));
+    }
     int clk;
     cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
     printf("{\"sms\": %d, \"clock_khz_attr\": %d, \"dadd_per_s\": %.4e, \"dfma_flops\": %.4e, \"lds64_bytes_per_s\": %.4e, "
