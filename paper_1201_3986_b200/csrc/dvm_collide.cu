@@ -412,7 +412,7 @@ void free_workspace(dvm_plan_s *P)
 {
     clear_profile(P);
     Workspace &w = P->ws;
-    void *ptrs[] = {w.S, w.part, w.f_stage, w.q_stage, w.mom_partial, w.mom_dev, w.qtmp, w.fft_z, w.g3_t, w.g3_q, w.g3_ctr};
+    void *ptrs[] = {w.S, w.part, w.f_stage, w.q_stage, w.mom_partial, w.mom_dev, w.qtmp, w.fft_z, w.g3_f, w.g3_t, w.g3_q, w.g3_ctr};
     for (void *q : ptrs)
         if (q) cudaFree(q);
     w = Workspace{};

@@ -34,10 +34,8 @@
 namespace dvm {
 namespace {
 
-constexpr int kGT = 512;        // threads per gain CTA (1 CTA per SM)
 constexpr int kCL = 16;         // CTAs per cell group
-constexpr int kMaxProg = 448;   // program entries (init + step) held in shared memory
-constexpr int kMeta = 24;       // ints of per-direction metadata
+constexpr int kMaxRec = 160;    // int4 words of a direction record (6 meta + program entries)
 constexpr int kMaxMS = 32;      // line half-width M_e held in shared memory
 constexpr int kFT = 256;        // FFT threads per CTA
 
@@ -54,6 +52,7 @@ struct FftArgs {
     // epilogue (last inverse pass): Q[c] = -f[c] * Λ[c]
     double *q;
     int64_t q_stride;
+    double2 *qI;  // epilogue, interleaved mode: qI[pair][node] = (-f_{2p} Λ_{2p}, -f_{2p+1} Λ_{2p+1})
     const double *f;
     int64_t f_stride;
     double scale;
@@ -137,7 +136,13 @@ __global__ void __launch_bounds__(kFT) k_fft_pass(FftArgs A)
             v.x *= m;
             v.y *= m;
         }
-        if (A.q) {
+        if (A.qI) {
+            const int64_t c0 = A.r_first + 2 * pair, c1 = c0 + 1;
+            double2 o;
+            o.x = -A.f[c0 * A.f_stride + a] * (v.x * A.scale);
+            o.y = c1 < A.r_cells ? -A.f[c1 * A.f_stride + a] * (v.y * A.scale) : 0.0;
+            A.qI[(A.r_first / 2 + pair) * nodes + a] = o;
+        } else if (A.q) {
             const int64_t c0 = A.r_first + 2 * pair, c1 = c0 + 1;
             A.q[c0 * A.q_stride + a] = -A.f[c0 * A.f_stride + a] * (v.x * A.scale);
             if (c1 < A.r_cells) A.q[c1 * A.q_stride + a] = -A.f[c1 * A.f_stride + a] * (v.y * A.scale);
@@ -198,38 +203,22 @@ __global__ void k_take_real(const double2 *z, int64_t n, double *out)
 
 // ------------------------------------------------------------------ gain
 struct GainArgs {
-    const double *f;
-    int64_t f_stride;
-    double *Q;  // accumulation target: [nchunks][ncells] blocks (see qc())
-    int64_t q_stride, q_chunk_stride;
-    int64_t ncells;
+    const double2 *f;   // [pairs][nodes]: cells 2p, 2p+1 interleaved
+    double2 *Q;         // [nchunks][pairs][nodes] interleaved accumulators (chunk 0 holds −fΛ)
+    int64_t npairs;
     int nchunks;
     int nloc;
-    const int *meta;    // [nloc][kMeta]
-    const int4 *prog;   // program entries
+    const int4 *rec;    // [nloc][recw]: 24 ints of frame metadata, then the program entries
+    int recw;
     const double *aw;   // [nloc]
-    double *Tbuf;       // [groups][2][nodes]
-    unsigned int *ctr;  // [groups] barrier counters
+    double2 *Tbuf;      // [groups][kSlots][nodes]
+    unsigned int *ctr;  // [groups][2][kCL]: steps completed by each CTA's phase A / phase B
     uint32_t H;
-    int p;
     int dbg;
 };
 
-__device__ __forceinline__ void group_barrier(unsigned int *ctr, unsigned int target)
-{
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(ctr, 1u);
-        unsigned int v;
-        for (;;) {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
-            if (v >= target) break;
-            __nanosleep(20);
-        }
-    }
-    __syncthreads();
-}
+constexpr int kSlots = 2;   // T ring depth per group (phase A may run kSlots-1 steps ahead)
+constexpr int kRoleT = 256; // threads per role (warps 0-7: phase A, warps 8-15: phase B)
 
 template <int N>
 __device__ __forceinline__ uint32_t pk(int c0, int c1, int c2)
@@ -238,283 +227,436 @@ __device__ __forceinline__ uint32_t pk(int c0, int c1, int c2)
     return ((uint32_t)(c0 & (N - 1)) << (2 * P)) | ((uint32_t)(c1 & (N - 1)) << P) | (uint32_t)(c2 & (N - 1));
 }
 
-// Shared-memory geometry of the gain kernel: planes are stored with L-1
-// duplicated rows (row N + k == row k) so that the L consecutive β-steps of a
-// thread address rows r0 .. r0 + L - 1 without wrap logic.
+__device__ __forceinline__ void role_sync(int id) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kRoleT) : "memory"); }
+
+// Wait until every CTA of the group has published progress >= target on its
+// own monotonic counter (ctrs[0..kCL)): lanes of the role's first warp poll one
+// counter each (acquire), then the role syncs.  Per-CTA counters, not a sum:
+// a CTA running ahead must not stand in for a slower one.
+__device__ __forceinline__ void role_wait(const unsigned int *ctrs, unsigned int target, int t, int id)
+{
+    if (t < 32) {
+        bool ok = t >= kCL;
+        for (;;) {
+            if (!ok) {
+                unsigned int v;
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctrs + t) : "memory");
+                ok = v >= target;
+            }
+            if (__all_sync(0xffffffffu, ok)) break;
+            __nanosleep(32);
+        }
+    }
+    role_sync(id);
+}
+
+// publish this CTA's role progress (all of the role's writes so far first)
+__device__ __forceinline__ void role_signal(unsigned int *own, unsigned int value, bool leader, int id)
+{
+    role_sync(id);
+    if (leader) {
+        __threadfence();
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(own), "r"(value) : "memory");
+    }
+}
+
+// ---- tensor memory (TMEM) as the phase-B accumulator store: each B-role thread
+// owns one TMEM lane and 256 32-bit columns (its 64 nodes × 2 cells in fp64).
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16])
+{
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16])
+{
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ double2 add2(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 sub2(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 fma2(double s, double2 a, double2 c)
+{
+    return make_double2(fma(s, a.x, c.x), fma(s, a.y, c.y));
+}
+
+// Shared-memory geometry (one lattice plane of a cell pair per slab).  Planes
+// keep L extra rows (row N + k == row k) so a thread's L consecutive β-steps
+// address rows r0 .. r0 + L - 1 without wrap logic.
 template <int N>
 struct G3Geom {
     static constexpr int LOGN = N == 32 ? 5 : 6;
-    static constexpr int NN = N * N;
-    static constexpr int SEGS = kGT / (2 * N);  // β segments per column
-    static constexpr int L = N / SEGS;           // outputs per segment
-    static constexpr int ROWS = N + L - 1;       // stored rows per plane
-    static constexpr int PL = ROWS * N;          // doubles per stored plane
-    static constexpr size_t smem = sizeof(double) * (4 * (size_t)PL + 2 * ROWS) + sizeof(int4) * kMaxProg +
+    static constexpr int SEGS = kRoleT / N;              // β segments per column
+    static constexpr int SEGLEN = N / SEGS;              // rows per segment
+    static constexpr int L = SEGLEN < 8 ? SEGLEN : 8;    // rows per register chunk
+    static constexpr int NCH = SEGLEN / L;
+    static constexpr int ROWS = N + L;
+    static constexpr int PL = ROWS * N;
+    static constexpr size_t smem = sizeof(double2) * (2 * (size_t)PL + ROWS) + sizeof(int4) * 2 * kMaxRec +
                                    sizeof(uint32_t) * 2 * kMaxMS;
 };
 
+// In-warp inclusive prefix (both cells) of one plane row held as v[h] at
+// α = lane + 32h; writes raw, prefix, total (and the duplicated row if row < L).
+template <int N, int L>
+__device__ __forceinline__ void row_store_scan2(const double2 (&v)[N / 32], int row, double2 *raw, double2 *pre,
+                                                double2 *tot, int lane)
+{
+    constexpr int H = N / 32;
+    double2 s[H];
+    double2 base = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+        double2 x = v[h];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double yx = __shfl_up_sync(0xffffffffu, x.x, o);
+            const double yy = __shfl_up_sync(0xffffffffu, x.y, o);
+            if (lane >= o) {
+                x.x += yx;
+                x.y += yy;
+            }
+        }
+        s[h] = add2(x, base);
+        base.x += __shfl_sync(0xffffffffu, x.x, 31);
+        base.y += __shfl_sync(0xffffffffu, x.y, 31);
+    }
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+        raw[row * N + lane + 32 * h] = v[h];
+        pre[row * N + lane + 32 * h] = s[h];
+        if (row < L) {
+            raw[(row + N) * N + lane + 32 * h] = v[h];
+            pre[(row + N) * N + lane + 32 * h] = s[h];
+        }
+    }
+    if (lane == 31) {
+        tot[row] = s[H - 1];
+        if (row < L) tot[row + N] = s[H - 1];
+    }
+}
+
 template <int N>
-__global__ void __launch_bounds__(kGT, 1) k_gain3d(GainArgs A)
+__global__ void __launch_bounds__(2 * kRoleT, 1) k_gain3d(GainArgs A)
 {
     using Gm = G3Geom<N>;
     constexpr int LOGN = Gm::LOGN;
-    constexpr int NN = Gm::NN;
     constexpr int64_t NODES = (int64_t)N * N * N;
     constexpr int SEGS = Gm::SEGS;
+    constexpr int SEGLEN = Gm::SEGLEN;
     constexpr int L = Gm::L;
-    constexpr int ROWS = Gm::ROWS;
-    constexpr int PL = Gm::PL;
-    constexpr int NPR = (int)(NODES / kCL);   // phase-B nodes per CTA
-    constexpr int GIT = 2 * NN / kGT;          // gathered nodes per thread per slab
+    constexpr int NCH = Gm::NCH;
+    constexpr int H = N / 32;
+    constexpr int NPR = (int)(NODES / kCL);  // phase-B nodes per CTA
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    double *raw = reinterpret_cast<double *>(smem_raw);   // [2][ROWS][N] (T overlays it after phase A3)
-    double *pre = raw + 2 * PL;                            // [2][ROWS][N] in-row prefix sums
-    double *tot = pre + 2 * PL;                            // [2][ROWS] row totals
-    int4 *sprog = reinterpret_cast<int4 *>(tot + 2 * ROWS);  // [kMaxProg]
-    uint32_t *soff = reinterpret_cast<uint32_t *>(sprog + kMaxProg);  // [2 * kMaxMS]
-    __shared__ int sm[kMeta];
+    double2 *raw = reinterpret_cast<double2 *>(smem_raw);  // [ROWS][N]
+    double2 *pre = raw + Gm::PL;                            // [ROWS][N] in-row prefix sums
+    double2 *tot = pre + Gm::PL;                            // [ROWS] row totals
+    int4 *srec = reinterpret_cast<int4 *>(tot + Gm::ROWS);  // [2][kMaxRec] double-buffered direction records
+    uint32_t *soff = reinterpret_cast<uint32_t *>(srec + 2 * kMaxRec);  // [2 * kMaxMS] (phase B)
+    __shared__ int smB[4];
 
-    const int tid = threadIdx.x;
+    const bool roleA = threadIdx.x < kRoleT;
+    const int t = threadIdx.x & (kRoleT - 1);
+    const int lane = t & 31, warp = t >> 5;
+    const bool leader = t == 0;
+    const int bar = roleA ? 1 : 2;
     const int rank = (int)(blockIdx.x % kCL);
     const int grp = (int)(blockIdx.x / kCL);
     const int ngroups = (int)(gridDim.x / kCL);
-    const uint32_t H = A.H;
-    unsigned int epoch = 0;
-    unsigned int step = 0;
-    const int64_t items = A.ncells * A.nchunks;
+    const uint32_t H2 = A.H;
+    unsigned int *cA = A.ctr + (size_t)grp * 2 * kCL, *cB = cA + kCL;
+    unsigned int stepi = 0;
+    const int64_t items = A.npairs * A.nchunks;
+
+    // TMEM: the B role's first warp allocates all 512 columns (one CTA per SM)
+    __shared__ uint32_t s_tmem;
+    if (!roleA && warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"l"(
+                         (uint64_t)__cvta_generic_to_shared(&s_tmem))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (!roleA) {
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        role_sync(2);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
+    // lane = 32 (warp % 4) + lane, columns: warps 8-11 -> [0, 256), 12-15 -> [256, 512)
+    const uint32_t tm_base = roleA ? 0u : (s_tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(256 * (warp >> 2)));
+
+    // direction records are double-buffered: the record of step s+1 is fetched
+    // into registers while step s runs and stored into the other buffer at its end
+    const int recw = A.recw;
+    int buf = 0;
+    int4 rnext = make_int4(0, 0, 0, 0);
+    int4 bnext0 = make_int4(0, 0, 0, 0), bnext3 = make_int4(0, 0, 0, 0);
+    if (grp < items) {
+        const int first_di = (int)((int64_t)A.nloc * (grp % A.nchunks) / A.nchunks);
+        if (roleA) {
+            for (int k = t; k < recw; k += kRoleT) srec[k] = A.rec[(int64_t)first_di * recw + k];
+        } else if (t == 0) {
+            bnext0 = A.rec[(int64_t)first_di * recw];
+            bnext3 = A.rec[(int64_t)first_di * recw + 3];
+        }
+        role_sync(bar);
+    }
 
     for (int64_t item = grp; item < items; item += ngroups) {
-        const int64_t cell = item / A.nchunks;
+        const int64_t pair = item / A.nchunks;
         const int chunk = (int)(item % A.nchunks);
         const int d0 = (int)((int64_t)A.nloc * chunk / A.nchunks);
         const int d1 = (int)((int64_t)A.nloc * (chunk + 1) / A.nchunks);
-        const double *__restrict__ fc = A.f + cell * A.f_stride;
-        double *Qc = A.Q + chunk * A.q_chunk_stride + cell * A.q_stride;
+        const double2 *__restrict__ fc = A.f + pair * NODES;
+        double2 *Qc = A.Q + ((int64_t)chunk * A.npairs + pair) * NODES;
 
-        for (int di = d0; di < d1; ++di, ++step) {
-            __syncthreads();  // previous direction's phase B done with sm/soff
-            if (tid < kMeta) sm[tid] = A.meta[di * kMeta + tid];
-            __syncthreads();
-            const int nprog = sm[16] + sm[17];
-            for (int k = tid; k < nprog && k < kMaxProg; k += kGT) sprog[k] = A.prog[sm[18] + k];
-            {
-                const int M = sm[15];
-                if (tid < 2 * M) {
-                    const int m = tid / 2 + 1, s = (tid & 1) ? -1 : 1;
-                    soff[tid] = pk<N>(s * m * sm[0], s * m * sm[1], s * m * sm[2]);
-                }
+        for (int di = d0; di < d1; ++di, ++stepi) {
+            double2 *Tb = A.Tbuf + ((int64_t)grp * kSlots + (stepi % kSlots)) * NODES;
+            int ndi = -1;  // the direction of this group's next step
+            if (di + 1 < d1) {
+                ndi = di + 1;
+            } else if (item + ngroups < items) {
+                const int nch = (int)((item + ngroups) % A.nchunks);
+                ndi = (int)((int64_t)A.nloc * nch / A.nchunks);
             }
-            __syncthreads();
-            double *Tb = A.Tbuf + ((int64_t)grp * 2 + (step & 1)) * NODES;
-
-            // ---------------------------------------------------------- phase A
-            if (!(A.dbg & 1)) {
-                const int z0 = sm[3], z1 = sm[4], z2 = sm[5];
-                const int u0 = sm[6], u1 = sm[7], u2 = sm[8];
-                const int w0 = sm[9], w1 = sm[10], w2 = sm[11];
-                const int a2 = sm[12], b2 = sm[13];
-                const int rows_mode = sm[14];
-                const int e2m = sm[2] & (N - 1);
-                const int ninit = sm[16], nstep = sm[17];
-                const int gg = rows_mode ? 1 : (e2m & -e2m);  // gcd(e2, N)
-                // per-thread gather/scatter pattern: GIT nodes, fixed column and plane,
-                // rows advancing by a constant (packed storage step sx)
-                int gj, gal, gbe0, gdbe;
-                if (rows_mode) {
-                    gj = 0;  // plane switches half-way (k >= GIT/2)
-                    gal = tid & (N - 1);
-                    gbe0 = tid >> LOGN;
-                    gdbe = kGT >> LOGN;
-                } else {
-                    gj = tid & 1;
-                    gal = (tid >> 1) & (N - 1);
-                    gbe0 = (tid >> 1) >> LOGN;
-                    gdbe = (kGT / 2) >> LOGN;
-                }
-                const uint32_t sx = pk<N>(gdbe * w0, gdbe * w1, gdbe * w2);
-                for (int s = rank; s < N / 2; s += kCL) {
-                    int g0, g1;
-                    if (rows_mode) {
-                        g0 = 2 * s;
-                        g1 = 2 * s + 1;
-                    } else {
-                        const int c = s % gg, i = s / gg;
-                        g0 = (c + 2 * i * e2m) & (N - 1);
-                        g1 = (g0 + e2m) & (N - 1);
-                    }
-                    // A1: gather (16-byte runs {x, x + ê_2}, or contiguous rows)
-                    {
-                        const int sal = rows_mode ? gal : ((gal + gj * a2) & (N - 1));
-                        const int g = g0;
-                        uint32_t x = pk<N>(g * z0 + gal * u0 + gbe0 * w0, g * z1 + gal * u1 + gbe0 * w1,
-                                           g * z2 + gal * u2 + gbe0 * w2 + (rows_mode ? 0 : gj));
-                        double v[GIT];
+            if (roleA) {
+                // ============================================ phase A: T_e -> slot
+                if (ndi >= 0 && t < recw) rnext = A.rec[(int64_t)ndi * recw + t];
+                if (stepi >= kSlots) role_wait(cB, stepi - kSlots + 1, t, bar);
+                const int *smA = reinterpret_cast<const int *>(srec + buf * kMaxRec);
+                const int4 *sprog = srec + buf * kMaxRec + 6;
+                const int z0 = smA[3], z1 = smA[4], z2 = smA[5];
+                const int u0 = smA[6], u1 = smA[7], u2 = smA[8];
+                const int w0 = smA[9], w1 = smA[10], w2 = smA[11];
+                const int ninit = smA[16], nstep = smA[17];
+                const uint32_t SW = pk<N>(w0, w1, w2);
+                uint32_t Uh[H];
 #pragma unroll
-                        for (int k = 0; k < GIT; ++k) {
-                            if (rows_mode && k == GIT / 2)
-                                x = pk<N>(g1 * z0 + gal * u0 + gbe0 * w0, g1 * z1 + gal * u1 + gbe0 * w1,
-                                          g1 * z2 + gal * u2 + gbe0 * w2);
-                            v[k] = __ldg(fc + x);
-                            x = swar_add(x, sx, H);
-                        }
+                for (int h = 0; h < H; ++h) Uh[h] = pk<N>((lane + 32 * h) * u0, (lane + 32 * h) * u1, (lane + 32 * h) * u2);
+                const int tal = t & (N - 1);
+                const int tbe = (t >> LOGN) * SEGLEN;
+                if (!(A.dbg & 1)) {
+                    for (int g = rank; g < N; g += kCL) {
+                        // A1: warp per row: gather the plane row (one 16-byte request per node,
+                        // both cells), prefix-scan it in registers, store raw + prefix rows
+                        if (!(A.dbg & 8)) {
+                            constexpr int NWA = kRoleT / 32;
+                            constexpr int RPW = N / NWA;           // rows per warp
+                            constexpr int RB = RPW > 4 ? 4 : RPW;  // rows per load batch
+#pragma unroll 1
+                            for (int k0 = 0; k0 < RPW; k0 += RB) {
+                                double2 v[RB][H];
 #pragma unroll
-                        for (int k = 0; k < GIT; ++k) {
-                            int j, row;
-                            if (rows_mode) {
-                                j = k >= GIT / 2;
-                                row = (gbe0 + (k % (GIT / 2)) * gdbe) & (N - 1);
-                            } else {
-                                j = gj;
-                                row = (gbe0 + k * gdbe + gj * b2) & (N - 1);
-                            }
-                            double *dst = raw + j * PL + row * N + sal;
-                            dst[0] = v[k];
-                            if (row < L - 1) dst[NN] = v[k];
-                        }
-                    }
-                    __syncthreads();
-                    // A2: in-row prefix sums of all stored rows (periodic rows; totals apart)
-                    {
-                        const int lane = tid & 31, warp = tid >> 5;
-                        constexpr int PLN = N / 32;
-                        for (int row = warp; row < 2 * ROWS; row += kGT / 32) {
-                            const double *src = raw + row * N;
-                            double v[PLN];
+                                for (int k = 0; k < RB; ++k) {
+                                    const int be = warp + NWA * (k0 + k);
+                                    const uint32_t B0 = pk<N>(g * z0 + be * w0, g * z1 + be * w1, g * z2 + be * w2);
 #pragma unroll
-                            for (int q = 0; q < PLN; ++q) v[q] = src[lane * PLN + q];
-#pragma unroll
-                            for (int q = 1; q < PLN; ++q) v[q] += v[q - 1];
-                            double x = v[PLN - 1];
-#pragma unroll
-                            for (int o = 1; o < 32; o <<= 1) {
-                                const double y = __shfl_up_sync(0xffffffffu, x, o);
-                                if (lane >= o) x += y;
-                            }
-                            const double excl = x - v[PLN - 1];
-                            double *dst = pre + row * N;
-#pragma unroll
-                            for (int q = 0; q < PLN; ++q) dst[lane * PLN + q] = v[q] + excl;
-                            if (lane == 31) tot[row] = x;
-                        }
-                    }
-                    __syncthreads();
-                    // A3: T by the sliding program; thread = (plane j, column al, β segment)
-                    {
-                        const int j = tid / (N * SEGS);
-                        const int rem = tid % (N * SEGS);
-                        const int al = rem & (N - 1), sg = rem >> LOGN;
-                        const double *R = raw + j * PL;
-                        const double *Pp = pre + j * PL;
-                        const double *Tt = tot + j * ROWS;
-                        const int be0 = sg * L;
-                        double T[L];
-                        {
-                            double acc = 0.0;
-                            for (int k = 0; k < ninit; ++k) {
-                                const int4 en = sprog[k];
-                                const int r0 = (be0 + en.x) & (N - 1);
-                                const int b = al + en.z, a = al + en.y - 1;
-                                double v = Pp[r0 * N + (b & (N - 1))] - Pp[r0 * N + (a & (N - 1))];
-                                if ((b >> LOGN) != (a >> LOGN)) v += Tt[r0];
-                                acc += v;
-                            }
-                            T[0] = acc;
-                        }
-#pragma unroll
-                        for (int q = 1; q < L; ++q) T[q] = 0.0;
-                        // T[q] (q >= 1) collects the step difference D(β0 + q − 1)
-                        for (int k = ninit; k < ninit + nstep; ++k) {
-                            const int4 en = sprog[k];
-                            const int r0 = (be0 + en.x) & (N - 1);
-                            const double sgn = (double)en.w;
-                            if (en.y == en.z) {
-                                const double *q0 = R + r0 * N + ((al + en.y) & (N - 1));
-#pragma unroll
-                                for (int q = 1; q < L; ++q) T[q] = fma(sgn, q0[(q - 1) * N], T[q]);
-                            } else {
-                                const int b = al + en.z, a = al + en.y - 1;
-                                const double *qb = Pp + r0 * N + (b & (N - 1));
-                                const double *qa = Pp + r0 * N + (a & (N - 1));
-                                if ((b >> LOGN) != (a >> LOGN)) {
-                                    const double *qt = Tt + r0;
-#pragma unroll
-                                    for (int q = 1; q < L; ++q)
-                                        T[q] = fma(sgn, (qb[(q - 1) * N] - qa[(q - 1) * N]) + qt[q - 1], T[q]);
-                                } else {
-#pragma unroll
-                                    for (int q = 1; q < L; ++q)
-                                        T[q] = fma(sgn, qb[(q - 1) * N] - qa[(q - 1) * N], T[q]);
+                                    for (int h = 0; h < H; ++h) v[k][h] = __ldg(fc + swar_add(B0, Uh[h], H2));
                                 }
+#pragma unroll
+                                for (int k = 0; k < RB; ++k)
+                                    row_store_scan2<N, L>(v[k], warp + NWA * (k0 + k), raw, pre, tot, lane);
                             }
                         }
+                        role_sync(bar);
+                        // A3: T by the sliding program (thread = column, β segment),
+                        // stored straight from registers (16 bytes per node)
+                        if (!(A.dbg & 4)) {
+                            const int al = tal;
+                            uint32_t x = pk<N>(g * z0 + al * u0 + tbe * w0, g * z1 + al * u1 + tbe * w1,
+                                               g * z2 + al * u2 + tbe * w2);
+                            double2 carry = make_double2(0.0, 0.0);
+#pragma unroll 1
+                            for (int c = 0; c < NCH; ++c) {
+                                const int be0 = tbe + c * L;
+                                double2 T[L + 1];
+                                if (c == 0) {
+                                    double2 acc = make_double2(0.0, 0.0);
+                                    for (int k = 0; k < ninit; ++k) {
+                                        const int4 en = sprog[k];
+                                        const int r0 = (be0 + en.x) & (N - 1);
+                                        const int b = al + en.z, a = al + en.y - 1;
+                                        double2 v = sub2(pre[r0 * N + (b & (N - 1))], pre[r0 * N + (a & (N - 1))]);
+                                        if ((b >> LOGN) != (a >> LOGN)) v = add2(v, tot[r0]);
+                                        acc = add2(acc, v);
+                                    }
+                                    T[0] = acc;
+                                } else {
+                                    T[0] = carry;
+                                }
 #pragma unroll
-                        for (int q = 1; q < L; ++q) T[q] += T[q - 1];
-                        __syncthreads();  // every thread is done reading raw: overlay T on it
-                        double *To = raw + j * PL + al;
+                                for (int q = 1; q <= L; ++q) T[q] = make_double2(0.0, 0.0);
+                                for (int k = ninit; k < ninit + nstep; ++k) {
+                                    const int4 en = sprog[k];
+                                    const int r0 = (be0 + en.x) & (N - 1);
+                                    const double sgn = (double)en.w;
+                                    if (en.y == en.z) {
+                                        const double2 *q0 = raw + r0 * N + ((al + en.y) & (N - 1));
 #pragma unroll
-                        for (int q = 0; q < L; ++q) To[(be0 + q) * N] = T[q];
+                                        for (int q = 1; q <= L; ++q) T[q] = fma2(sgn, q0[(q - 1) * N], T[q]);
+                                    } else {
+                                        const int b = al + en.z, a = al + en.y - 1;
+                                        const double2 *qb = pre + r0 * N + (b & (N - 1));
+                                        const double2 *qa = pre + r0 * N + (a & (N - 1));
+                                        if ((b >> LOGN) != (a >> LOGN)) {
+                                            const double2 *qt = tot + r0;
+#pragma unroll
+                                            for (int q = 1; q <= L; ++q)
+                                                T[q] = fma2(sgn, add2(sub2(qb[(q - 1) * N], qa[(q - 1) * N]), qt[q - 1]), T[q]);
+                                        } else {
+#pragma unroll
+                                            for (int q = 1; q <= L; ++q)
+                                                T[q] = fma2(sgn, sub2(qb[(q - 1) * N], qa[(q - 1) * N]), T[q]);
+                                        }
+                                    }
+                                }
+#pragma unroll
+                                for (int q = 1; q <= L; ++q) T[q] = add2(T[q], T[q - 1]);
+#pragma unroll
+                                for (int q = 0; q < L; ++q) {
+                                    __stcg(Tb + x, T[q]);
+                                    x = swar_add(x, SW, H2);
+                                }
+                                carry = T[L];
+                            }
+                        }
+                        role_sync(bar);  // raw/pre free for the next plane
                     }
-                    __syncthreads();
-                    // A4: write T back in storage order (same runs as the gather)
-                    {
-                        const int sal = rows_mode ? gal : ((gal + gj * a2) & (N - 1));
-                        uint32_t x = pk<N>(g0 * z0 + gal * u0 + gbe0 * w0, g0 * z1 + gal * u1 + gbe0 * w1,
-                                           g0 * z2 + gal * u2 + gbe0 * w2 + (rows_mode ? 0 : gj));
+                }
+                if (ndi >= 0 && t < recw) srec[(buf ^ 1) * kMaxRec + t] = rnext;
+                buf ^= 1;
+                role_signal(cA + rank, stepi + 1, leader, bar);
+            } else {
+                // ============================================ phase B: Q += a_e T_e S_e
+                if (t == 0) {
+                    smB[0] = bnext0.x;
+                    smB[1] = bnext0.y;
+                    smB[2] = bnext0.z;
+                    smB[3] = bnext3.w;  // M_e
+                    if (ndi >= 0) {
+                        bnext0 = A.rec[(int64_t)ndi * recw];
+                        bnext3 = A.rec[(int64_t)ndi * recw + 3];
+                    }
+                }
+                role_wait(cA, stepi + 1, t, bar);
+                const int M = smB[3];
+                if (t < 2 * M) {
+                    const int m = t / 2 + 1, sg = (t & 1) ? -1 : 1;
+                    soff[t] = pk<N>(sg * m * smB[0], sg * m * smB[1], sg * m * smB[2]);
+                }
+                role_sync(bar);
+                if (!(A.dbg & 2)) {
+                    // thread-owned nodes n0 + t + 256 j (j < NPR/256), accumulated in TMEM:
+                    // 4 nodes (8 doubles, 16 columns) per batch
+                    constexpr int NB = 4;
+                    constexpr int NJ = NPR / kRoleT;
+                    static_assert(NJ % NB == 0, "phase-B tiling");
+                    const bool first = di == d0, last = di == d1 - 1;
+                    const double aw = A.aw[di];
+                    const int M2 = 2 * M;
+                    const uint32_t n0 = (uint32_t)rank * NPR + t;
+#pragma unroll 1
+                    for (int j0 = 0; j0 < NJ; j0 += NB) {
+                        uint32_t n[NB];
+                        double2 T[NB], S[NB];
 #pragma unroll
-                        for (int k = 0; k < GIT; ++k) {
-                            int j, row;
-                            if (rows_mode) {
-                                if (k == GIT / 2)
-                                    x = pk<N>(g1 * z0 + gal * u0 + gbe0 * w0, g1 * z1 + gal * u1 + gbe0 * w1,
-                                              g1 * z2 + gal * u2 + gbe0 * w2);
-                                j = k >= GIT / 2;
-                                row = (gbe0 + (k % (GIT / 2)) * gdbe) & (N - 1);
+                        for (int b = 0; b < NB; ++b) {
+                            n[b] = n0 + (uint32_t)(j0 + b) * kRoleT;
+                            T[b] = __ldcg(Tb + n[b]);
+                            S[b] = make_double2(0.0, 0.0);
+                        }
+                        for (int k = 0; k < M2; ++k) {
+                            const uint32_t off = soff[k];
+#pragma unroll
+                            for (int b = 0; b < NB; ++b) S[b] = add2(S[b], __ldg(fc + swar_add(n[b], off, H2)));
+                        }
+                        uint32_t r[16];
+                        const uint32_t ta = tm_base + (uint32_t)(4 * j0);
+                        if (first) {
+#pragma unroll
+                            for (int b = 0; b < NB; ++b) {
+                                const double2 q = __ldcg(Qc + n[b]);  // −fΛ (chunk 0) or 0
+                                r[4 * b + 0] = __double2loint(q.x);
+                                r[4 * b + 1] = __double2hiint(q.x);
+                                r[4 * b + 2] = __double2loint(q.y);
+                                r[4 * b + 3] = __double2hiint(q.y);
+                            }
+                        } else {
+                            tmem_ld16(ta, r);
+                        }
+#pragma unroll
+                        for (int b = 0; b < NB; ++b) {
+                            double qx = __hiloint2double(r[4 * b + 1], r[4 * b + 0]);
+                            double qy = __hiloint2double(r[4 * b + 3], r[4 * b + 2]);
+                            qx += aw * T[b].x * S[b].x;
+                            qy += aw * T[b].y * S[b].y;
+                            if (last) {
+                                Qc[n[b]] = make_double2(qx, qy);
                             } else {
-                                j = gj;
-                                row = (gbe0 + k * gdbe + gj * b2) & (N - 1);
+                                r[4 * b + 0] = __double2loint(qx);
+                                r[4 * b + 1] = __double2hiint(qx);
+                                r[4 * b + 2] = __double2loint(qy);
+                                r[4 * b + 3] = __double2hiint(qy);
                             }
-                            __stcg(Tb + x, raw[j * PL + row * N + sal]);
-                            x = swar_add(x, sx, H);
                         }
+                        if (!last) tmem_st16(ta, r);
                     }
-                    // (the next slab's A1 rewrites raw only after every thread passed A4:
-                    //  A1 of the next slab is separated by the barrier below)
-                    __syncthreads();
+                    tmem_wait_st();
                 }
-            }
-            ++epoch;
-            group_barrier(A.ctr + grp, epoch * (unsigned)kCL);
-
-            // ---------------------------------------------------------- phase B
-            if (!(A.dbg & 2)) {
-                constexpr int NB = (NPR / kGT) < 8 ? (NPR / kGT) : 8;
-                static_assert(NPR % (kGT * NB) == 0, "phase-B tiling");
-                const double aw = A.aw[di];
-                const int M2 = 2 * sm[15];
-                const uint32_t n0 = (uint32_t)rank * NPR;
-                for (int i0 = tid; i0 < NPR; i0 += kGT * NB) {
-                    uint32_t n[NB];
-                    double T[NB], S[NB];
-#pragma unroll
-                    for (int b = 0; b < NB; ++b) {
-                        n[b] = n0 + i0 + b * kGT;
-                        T[b] = __ldcg(Tb + n[b]);
-                        S[b] = 0.0;
-                    }
-                    for (int k = 0; k < M2; ++k) {
-                        const uint32_t off = soff[k];
-#pragma unroll
-                        for (int b = 0; b < NB; ++b) S[b] += __ldg(fc + swar_add(n[b], off, H));
-                    }
-#pragma unroll
-                    for (int b = 0; b < NB; ++b) Qc[n[b]] += aw * T[b] * S[b];
-                }
+                role_signal(cB + rank, stepi + 1, leader, bar);
             }
         }
+    }
+    if (!roleA) {
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        role_sync(2);
+        if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(s_tmem) : "memory");
+    }
+}
+
+// f [cells][stride] -> fI [pairs][nodes] (double2), odd tail padded with 0
+__global__ void k_interleave(const double *__restrict__ f, int64_t stride, int64_t ncells, int64_t nodes,
+                             double2 *__restrict__ fI)
+{
+    const int64_t npairs = (ncells + 1) / 2;
+    const int64_t total = npairs * nodes;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = i / nodes, x = i % nodes;
+        const int64_t c0 = 2 * p, c1 = c0 + 1;
+        fI[i] = make_double2(f[c0 * stride + x], c1 < ncells ? f[c1 * stride + x] : 0.0);
+    }
+}
+
+// Q[cell] = Σ_chunks QI[chunk][pair][.] component (chunk order: deterministic)
+__global__ void k_deinterleave(const double2 *__restrict__ QI, int nchunks, int64_t npairs, int64_t ncells,
+                               int64_t nodes, double *__restrict__ Q, int64_t stride)
+{
+    const int64_t total = ncells * nodes;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = i / nodes, x = i % nodes;
+        const int64_t p = c / 2;
+        const bool hi = c & 1;
+        double acc = 0.0;
+        for (int k = 0; k < nchunks; ++k) {
+            const double2 v = QI[((int64_t)k * npairs + p) * nodes + x];
+            acc += hi ? v.y : v.x;
+        }
+        Q[c * stride + x] = acc;
     }
 }
 
 size_t gain_smem_bytes(int N) { return N == 32 ? G3Geom<32>::smem : G3Geom<64>::smem; }
+
 
 template <typename T>
 dvm_status_t grow(T **ptr, size_t *cap, size_t need, cudaStream_t s)
@@ -560,7 +702,8 @@ dvm_status_t fft_dispatch(dvm_plan_s *P, const FftArgs &a)
 }
 
 // Loss initialisation Q[c] := −f[c] Λ[c] for cells [0, ncells) (Λ = λ ⊛ f).
-dvm_status_t loss_init(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q, int64_t q_stride, int64_t ncells)
+dvm_status_t loss_init(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q, int64_t q_stride, int64_t ncells,
+                       double2 *QI = nullptr)
 {
     const int d = P->d;
     int64_t nodes = 1;
@@ -591,6 +734,7 @@ dvm_status_t loss_init(dvm_plan_s *P, const double *f, int64_t f_stride, double 
             }
             if (k == d - 1) a.mult = P->g.lamhat;
             if (k == 2 * d - 1) {
+                a.qI = QI;
                 a.q = Q;
                 a.q_stride = q_stride;
                 a.f = f;
@@ -614,7 +758,7 @@ dvm_status_t launch_gain(dvm_plan_s *P, const double *f, int64_t f_stride, doubl
     DVM_CUDA(cudaGetDevice(&dev));
     DVM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     DVM_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
-    DVM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kGT, smem));
+    DVM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 2 * kRoleT, smem));
     if (!coop || per_sm < 1) {
         set_error("gain3d kernel cannot be launched cooperatively on this device");
         return DVM_E_CUDA;
@@ -623,43 +767,41 @@ dvm_status_t launch_gain(dvm_plan_s *P, const double *f, int64_t f_stride, doubl
     if (getenv("DVM_G3_GROUPS")) max_groups = std::max(1, std::min(max_groups, atoi(getenv("DVM_G3_GROUPS"))));
     const int nloc = (int)P->local.size();
     const int64_t nodes = (int64_t)N * N * N;
+    const int64_t npairs = (ncells + 1) / 2;
     int nchunks = 1;
-    if (ncells < max_groups) nchunks = (int)std::min<int64_t>(nloc, max_groups / ncells);
+    if (npairs < max_groups) nchunks = (int)std::min<int64_t>(std::max(1, nloc), max_groups / npairs);
     nchunks = std::max(1, nchunks);
-    const int64_t items = ncells * nchunks;
+    const int64_t items = npairs * nchunks;
     const int ngroups = (int)std::min<int64_t>(max_groups, items);
     Workspace &w = P->ws;
     dvm_status_t st;
-    if ((st = grow(&w.g3_t, &w.g3_t_elems, (size_t)ngroups * 2 * nodes, P->stream))) return st;
-    if ((st = grow(&w.g3_ctr, &w.g3_ctr_elems, (size_t)ngroups, P->stream))) return st;
-    double *Qacc = Q;
-    int64_t qs = q_stride, qcs = 0;
-    if (nchunks > 1) {
-        if ((st = grow(&w.g3_q, &w.g3_q_elems, (size_t)nchunks * ncells * nodes, P->stream))) return st;
-        Qacc = w.g3_q;
-        qs = nodes;
-        qcs = ncells * nodes;
-        DVM_CUDA(cudaMemsetAsync(w.g3_q + qcs, 0, sizeof(double) * (size_t)(nchunks - 1) * qcs, P->stream));
+    if ((st = grow(&w.g3_f, &w.g3_f_elems, (size_t)(npairs * nodes), P->stream))) return st;
+    if ((st = grow(&w.g3_q, &w.g3_q_elems, (size_t)(nchunks * npairs * nodes), P->stream))) return st;
+    if ((st = grow(&w.g3_t, &w.g3_t_elems, (size_t)ngroups * kSlots * nodes, P->stream))) return st;
+    if ((st = grow(&w.g3_ctr, &w.g3_ctr_elems, (size_t)ngroups * 2 * kCL, P->stream))) return st;
+    {
+        LaunchScope ls(P, KC_ZERO);
+        k_interleave<<<1184, 256, 0, P->stream>>>(f, f_stride, ncells, nodes, w.g3_f);
+        DVM_CUDA(cudaGetLastError());
     }
-    // loss first: Q_acc(chunk 0) := −f Λ
-    if ((st = loss_init(P, f, f_stride, Qacc, qs, ncells))) return st;
-    DVM_CUDA(cudaMemsetAsync(w.g3_ctr, 0, sizeof(unsigned int) * ngroups, P->stream));
+    if (nchunks > 1)
+        DVM_CUDA(cudaMemsetAsync(w.g3_q + npairs * nodes, 0, sizeof(double2) * (size_t)((nchunks - 1) * npairs * nodes),
+                                 P->stream));
+    // loss first: chunk 0 := −f Λ (interleaved)
+    if ((st = loss_init(P, f, f_stride, nullptr, 0, ncells, w.g3_q))) return st;
+    DVM_CUDA(cudaMemsetAsync(w.g3_ctr, 0, sizeof(unsigned int) * 2 * kCL * ngroups, P->stream));
     GainArgs a;
-    a.f = f;
-    a.f_stride = f_stride;
-    a.Q = Qacc;
-    a.q_stride = qs;
-    a.q_chunk_stride = qcs;
-    a.ncells = ncells;
+    a.f = w.g3_f;
+    a.Q = w.g3_q;
+    a.npairs = npairs;
     a.nchunks = nchunks;
     a.nloc = nloc;
-    a.meta = P->g.meta;
-    a.prog = P->g.prog;
+    a.rec = P->g.rec;
+    a.recw = P->g.recw;
     a.aw = P->g.aw;
     a.Tbuf = w.g3_t;
     a.ctr = w.g3_ctr;
     a.H = P->pk.H;
-    a.p = P->p;
     a.dbg = getenv("DVM_G3_DEBUG") ? atoi(getenv("DVM_G3_DEBUG")) : 0;
     if (getenv("DVM_VERBOSE"))
         fprintf(stderr, "[dvm] gain3d N=%d: %d groups x %d CTAs, %d chunks, smem %zu\n", N, ngroups, kCL, nchunks,
@@ -667,11 +809,12 @@ dvm_status_t launch_gain(dvm_plan_s *P, const double *f, int64_t f_stride, doubl
     {
         void *args[] = {&a};
         LaunchScope ls(P, KC_GAIN3D);
-        DVM_CUDA(cudaLaunchCooperativeKernel((void *)kern, dim3(ngroups * kCL), dim3(kGT), args, smem, P->stream));
+        DVM_CUDA(cudaLaunchCooperativeKernel((void *)kern, dim3(ngroups * kCL), dim3(2 * kRoleT), args, smem, P->stream));
     }
-    if (nchunks > 1) {
-        if ((st = zero_cells(P, Q, q_stride, ncells, nodes))) return st;
-        if ((st = reduce_slots(P, Q, q_stride, w.g3_q, ncells * nodes, nchunks, ncells, nodes))) return st;
+    {
+        LaunchScope ls(P, KC_REDUCE);
+        k_deinterleave<<<1184, 256, 0, P->stream>>>(w.g3_q, nchunks, npairs, ncells, nodes, Q, q_stride);
+        DVM_CUDA(cudaGetLastError());
     }
     return DVM_OK;
 }
@@ -685,22 +828,34 @@ dvm_status_t build_gain3d(dvm_plan_s *P)
     if (P->d != 3 || (P->N != 32 && P->N != 64)) return DVM_OK;
     const int nloc = (int)P->local.size();
     const int N = P->N;
-    const int SEGS = kGT / (2 * N), L = N / SEGS;
-    std::vector<int> meta((size_t)std::max(1, nloc) * kMeta, 0);
-    std::vector<int4> prog;
+    const int L = N == 32 ? G3Geom<32>::SEGLEN : G3Geom<64>::SEGLEN;
+    std::vector<frame::DirFrame> frames(nloc);
     std::vector<double> aw(std::max(1, nloc), 0.0);
+    int maxent = 0;
     for (int k = 0; k < nloc; ++k) {
         const int di = P->local[k];
-        frame::DirFrame F;
+        frame::DirFrame &F = frames[k];
         if (!frame::build_dir(&P->h_e[3 * di], P->Ntilde, N, L, F)) {
             set_error("gain3d: no frame for a direction");
             return DVM_E_UNSUPPORTED;
         }
-        if ((int)(F.init.size() + F.step.size()) > kMaxProg || F.M > kMaxMS / 2) {
-            set_error("gain3d: direction program exceeds the shared-memory table");
+        maxent = std::max(maxent, (int)(F.init.size() + F.step.size()));
+        if (F.M > kMaxMS / 2) {
+            set_error("gain3d: line half-width exceeds the shared-memory table");
             return DVM_E_UNSUPPORTED;
         }
-        int *m = &meta[(size_t)k * kMeta];
+        aw[k] = P->h_a[di];
+    }
+    // fixed-size direction records: 6 int4 of metadata + program entries
+    const int recw = 6 + maxent;
+    if (recw > kMaxRec) {
+        set_error("gain3d: direction program exceeds the shared-memory record");
+        return DVM_E_UNSUPPORTED;
+    }
+    std::vector<int4> rec((size_t)std::max(1, nloc) * recw, make_int4(0, 0, 0, 0));
+    for (int k = 0; k < nloc; ++k) {
+        const frame::DirFrame &F = frames[k];
+        int m[24] = {0};
         for (int j = 0; j < 3; ++j) {
             m[j] = F.e[j];
             m[3 + j] = F.z[j];
@@ -713,23 +868,22 @@ dvm_status_t build_gain3d(dvm_plan_s *P)
         m[15] = F.M;
         m[16] = (int)F.init.size();
         m[17] = (int)F.step.size();
-        m[18] = (int)prog.size();
-        for (const auto &x : F.init) prog.push_back(make_int4(x.rho, x.t1, x.t2, x.sign));
-        for (const auto &x : F.step) prog.push_back(make_int4(x.rho, x.t1, x.t2, x.sign));
-        aw[k] = P->h_a[di];
+        int4 *r = &rec[(size_t)k * recw];
+        for (int q = 0; q < 6; ++q) r[q] = make_int4(m[4 * q], m[4 * q + 1], m[4 * q + 2], m[4 * q + 3]);
+        int q = 6;
+        for (const auto &x : F.init) r[q++] = make_int4(x.rho, x.t1, x.t2, x.sign);
+        for (const auto &x : F.step) r[q++] = make_int4(x.rho, x.t1, x.t2, x.sign);
     }
-    if (prog.empty()) prog.push_back(make_int4(0, 0, 0, 0));
     GainTables &g = P->g;
-    DVM_CUDA(cudaMalloc(&g.meta, sizeof(int) * meta.size()));
-    DVM_CUDA(cudaMalloc(&g.prog, sizeof(int4) * prog.size()));
+    g.recw = recw;
+    DVM_CUDA(cudaMalloc(&g.rec, sizeof(int4) * rec.size()));
     DVM_CUDA(cudaMalloc(&g.aw, sizeof(double) * aw.size()));
     DVM_CUDA(cudaMalloc(&g.tw, sizeof(double2) * N / 2));
     const int64_t nodes = (int64_t)N * N * N;
     DVM_CUDA(cudaMalloc(&g.lamhat, sizeof(double) * nodes));
-    g.bytes = sizeof(int) * meta.size() + sizeof(int4) * prog.size() + sizeof(double) * aw.size() +
-              sizeof(double2) * N / 2 + sizeof(double) * nodes;
-    DVM_CUDA(cudaMemcpyAsync(g.meta, meta.data(), sizeof(int) * meta.size(), cudaMemcpyHostToDevice, P->stream));
-    DVM_CUDA(cudaMemcpyAsync(g.prog, prog.data(), sizeof(int4) * prog.size(), cudaMemcpyHostToDevice, P->stream));
+    g.bytes = sizeof(int4) * rec.size() + sizeof(double) * aw.size() + sizeof(double2) * N / 2 +
+              sizeof(double) * nodes;
+    DVM_CUDA(cudaMemcpyAsync(g.rec, rec.data(), sizeof(int4) * rec.size(), cudaMemcpyHostToDevice, P->stream));
     DVM_CUDA(cudaMemcpyAsync(g.aw, aw.data(), sizeof(double) * aw.size(), cudaMemcpyHostToDevice, P->stream));
     {
         LaunchScope ls(P, KC_PLAN);
@@ -779,7 +933,7 @@ dvm_status_t build_gain3d(dvm_plan_s *P)
 void free_gain3d(dvm_plan_s *P)
 {
     GainTables &g = P->g;
-    void *ptrs[] = {g.meta, g.prog, g.aw, g.tw, g.lamhat};
+    void *ptrs[] = {g.rec, g.aw, g.tw, g.lamhat};
     for (void *q : ptrs)
         if (q) cudaFree(q);
     g = GainTables{};

@@ -70,10 +70,11 @@ struct Workspace {
     size_t mom_rows = 0;
     double *qtmp = nullptr;         // euler scratch (nodes)
     double2 *fft_z = nullptr;       // 3D loss: complex FFT workspace [pairs][nodes]
-    double *g3_t = nullptr;         // 3D gain: per-group ping-pong T_e buffers [groups][2][nodes]
-    double *g3_q = nullptr;         // 3D gain: per-chunk partial Q (small batches)
+    double2 *g3_f = nullptr;        // 3D gain: cell pairs of f, interleaved [pairs][nodes]
+    double2 *g3_t = nullptr;        // 3D gain: per-group ring of T_e buffers [groups][slots][nodes]
+    double2 *g3_q = nullptr;        // 3D gain: interleaved Q accumulators [chunks][pairs][nodes]
     unsigned int *g3_ctr = nullptr; // 3D gain: group barrier counters
-    size_t fft_z_elems = 0, g3_t_elems = 0, g3_q_elems = 0, g3_ctr_elems = 0;
+    size_t fft_z_elems = 0, g3_f_elems = 0, g3_t_elems = 0, g3_q_elems = 0, g3_ctr_elems = 0;
 };
 
 }  // namespace dvm
@@ -90,8 +91,8 @@ namespace dvm {
 // Plan tables of the 3D gain/loss path (dvm_gain3d.cu, dvm_frame.h).
 struct GainTables {
     bool ready = false;
-    int *meta = nullptr;      // [A_local][24] frame + program header per local direction
-    int4 *prog = nullptr;     // sliding-program entries (rho, t1, t2, sign)
+    int4 *rec = nullptr;      // [A_local][recw] frame metadata (6 int4) + sliding-program entries
+    int recw = 0;
     double *aw = nullptr;     // [A_local] a_e
     double2 *tw = nullptr;    // FFT twiddles exp(-2πik/N), k < N/2
     double *lamhat = nullptr; // [N^3] spectrum of the loss kernel λ (real)
