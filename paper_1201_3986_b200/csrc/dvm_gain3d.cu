@@ -35,7 +35,7 @@ namespace dvm {
 namespace {
 
 constexpr int kCL = 16;         // CTAs per cell group
-constexpr int kMaxRec = 160;    // int4 words of a direction record (6 meta + program entries)
+constexpr int kMaxRec = 72;     // int4 words of a direction record (6 meta + program entries)
 constexpr int kMaxMS = 32;      // line half-width M_e held in shared memory
 constexpr int kFT = 256;        // FFT threads per CTA
 
@@ -290,9 +290,12 @@ __device__ __forceinline__ double2 fma2(double s, double2 a, double2 c)
     return make_double2(fma(s, a.x, c.x), fma(s, a.y, c.y));
 }
 
-// Shared-memory geometry (one lattice plane of a cell pair per slab).  Planes
-// keep L extra rows (row N + k == row k) so a thread's L consecutive β-steps
-// address rows r0 .. r0 + L - 1 without wrap logic.
+// Shared-memory geometry (one lattice plane of a cell pair at a time).  Rows
+// are padded to RS = N + 1 double2 (a thread-per-row scan is then bank-conflict
+// free) and planes keep L extra rows (row N + k == row k) so a thread's L
+// consecutive β-steps address rows r0 .. r0 + L - 1 without wrap logic.  The
+// raw plane is double-buffered: the next plane is gathered by cp.async while
+// the current one is scanned and evaluated.
 template <int N>
 struct G3Geom {
     static constexpr int LOGN = N == 32 ? 5 : 6;
@@ -301,49 +304,44 @@ struct G3Geom {
     static constexpr int L = SEGLEN < 8 ? SEGLEN : 8;    // rows per register chunk
     static constexpr int NCH = SEGLEN / L;
     static constexpr int ROWS = N + L;
-    static constexpr int PL = ROWS * N;
-    static constexpr size_t smem = sizeof(double2) * (2 * (size_t)PL + ROWS) + sizeof(int4) * 2 * kMaxRec +
+    static constexpr int RS = N + 1;
+    static constexpr int PL = ROWS * RS;
+    static constexpr int NPL = N / kCL;                  // planes per CTA per direction
+    static constexpr size_t smem = sizeof(double2) * (3 * (size_t)PL + ROWS) + sizeof(int4) * 2 * kMaxRec +
                                    sizeof(uint32_t) * 2 * kMaxMS;
 };
 
-// In-warp inclusive prefix (both cells) of one plane row held as v[h] at
-// α = lane + 32h; writes raw, prefix, total (and the duplicated row if row < L).
-template <int N, int L>
-__device__ __forceinline__ void row_store_scan2(const double2 (&v)[N / 32], int row, double2 *raw, double2 *pre,
-                                                double2 *tot, int lane)
+__device__ __forceinline__ void cp_async16(void *smem_dst, const void *gsrc)
 {
-    constexpr int H = N / 32;
-    double2 s[H];
-    double2 base = make_double2(0.0, 0.0);
-#pragma unroll
-    for (int h = 0; h < H; ++h) {
-        double2 x = v[h];
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const double yx = __shfl_up_sync(0xffffffffu, x.x, o);
-            const double yy = __shfl_up_sync(0xffffffffu, x.y, o);
-            if (lane >= o) {
-                x.x += yx;
-                x.y += yy;
-            }
-        }
-        s[h] = add2(x, base);
-        base.x += __shfl_sync(0xffffffffu, x.x, 31);
-        base.y += __shfl_sync(0xffffffffu, x.y, 31);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem_dst)),
+                 "l"(gsrc)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// Gather lattice plane g (frame z, u, w) of a cell pair into dst[ROWS][RS]
+// (rows < L also into their duplicate rows) with 16-byte cp.async requests.
+template <int N>
+__device__ __forceinline__ void gather_plane(const double2 *fcp, double2 *dst, int g, const int *zuw, int t,
+                                             uint32_t H2)
+{
+    using Gm = G3Geom<N>;
+    constexpr int DB = kRoleT / N;  // rows advanced per pass
+    const int al = t & (N - 1);
+    int be = t >> Gm::LOGN;
+    const int z0 = zuw[0], z1 = zuw[1], z2 = zuw[2], u0 = zuw[3], u1 = zuw[4], u2 = zuw[5];
+    const int w0 = zuw[6], w1 = zuw[7], w2 = zuw[8];
+    uint32_t x = pk<N>(g * z0 + al * u0 + be * w0, g * z1 + al * u1 + be * w1, g * z2 + al * u2 + be * w2);
+    const uint32_t sx = pk<N>(DB * w0, DB * w1, DB * w2);
+#pragma unroll 4
+    for (int k = 0; k < N / DB; ++k) {
+        cp_async16(dst + be * Gm::RS + al, fcp + x);
+        if (be < Gm::L) cp_async16(dst + (be + N) * Gm::RS + al, fcp + x);
+        be += DB;
+        x = swar_add(x, sx, H2);
     }
-#pragma unroll
-    for (int h = 0; h < H; ++h) {
-        raw[row * N + lane + 32 * h] = v[h];
-        pre[row * N + lane + 32 * h] = s[h];
-        if (row < L) {
-            raw[(row + N) * N + lane + 32 * h] = v[h];
-            pre[(row + N) * N + lane + 32 * h] = s[h];
-        }
-    }
-    if (lane == 31) {
-        tot[row] = s[H - 1];
-        if (row < L) tot[row + N] = s[H - 1];
-    }
+    cp_async_commit();
 }
 
 template <int N>
@@ -359,9 +357,11 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_gain3d(GainArgs A)
     constexpr int H = N / 32;
     constexpr int NPR = (int)(NODES / kCL);  // phase-B nodes per CTA
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    double2 *raw = reinterpret_cast<double2 *>(smem_raw);  // [ROWS][N]
-    double2 *pre = raw + Gm::PL;                            // [ROWS][N] in-row prefix sums
-    double2 *tot = pre + Gm::PL;                            // [ROWS] row totals
+    constexpr int RS = Gm::RS;
+    constexpr int NPL = Gm::NPL;
+    double2 *rawb = reinterpret_cast<double2 *>(smem_raw);  // [2][ROWS][RS] gathered planes
+    double2 *pre = rawb + 2 * Gm::PL;                        // [ROWS][RS] in-row prefix sums
+    double2 *tot = pre + Gm::PL;                             // [ROWS] row totals
     int4 *srec = reinterpret_cast<int4 *>(tot + Gm::ROWS);  // [2][kMaxRec] double-buffered direction records
     uint32_t *soff = reinterpret_cast<uint32_t *>(srec + 2 * kMaxRec);  // [2 * kMaxMS] (phase B)
     __shared__ int smB[4];
@@ -401,10 +401,15 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_gain3d(GainArgs A)
     int buf = 0;
     int4 rnext = make_int4(0, 0, 0, 0);
     int4 bnext0 = make_int4(0, 0, 0, 0), bnext3 = make_int4(0, 0, 0, 0);
+    int cur = 0;  // raw plane buffer holding the next plane to evaluate
     if (grp < items) {
         const int first_di = (int)((int64_t)A.nloc * (grp % A.nchunks) / A.nchunks);
         if (roleA) {
             for (int k = t; k < recw; k += kRoleT) srec[k] = A.rec[(int64_t)first_di * recw + k];
+            role_sync(bar);
+            // first plane of the first step
+            gather_plane<N>(A.f + (grp / A.nchunks) * NODES, rawb, rank, reinterpret_cast<const int *>(srec) + 3, t,
+                            H2);
         } else if (t == 0) {
             bnext0 = A.rec[(int64_t)first_di * recw];
             bnext3 = A.rec[(int64_t)first_di * recw + 3];
@@ -440,100 +445,101 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_gain3d(GainArgs A)
                 const int w0 = smA[9], w1 = smA[10], w2 = smA[11];
                 const int ninit = smA[16], nstep = smA[17];
                 const uint32_t SW = pk<N>(w0, w1, w2);
-                uint32_t Uh[H];
-#pragma unroll
-                for (int h = 0; h < H; ++h) Uh[h] = pk<N>((lane + 32 * h) * u0, (lane + 32 * h) * u1, (lane + 32 * h) * u2);
                 const int tal = t & (N - 1);
                 const int tbe = (t >> LOGN) * SEGLEN;
-                if (!(A.dbg & 1)) {
-                    for (int g = rank; g < N; g += kCL) {
-                        // A1: warp per row: gather the plane row (one 16-byte request per node,
-                        // both cells), prefix-scan it in registers, store raw + prefix rows
-                        if (!(A.dbg & 8)) {
-                            constexpr int NWA = kRoleT / 32;
-                            constexpr int RPW = N / NWA;           // rows per warp
-                            constexpr int RB = RPW > 4 ? 4 : RPW;  // rows per load batch
+                // cell pair of the next step (prefetch target of the last plane)
+                const double2 *fnext = (di + 1 < d1) ? fc : A.f + ((item + ngroups) / A.nchunks) * NODES;
 #pragma unroll 1
-                            for (int k0 = 0; k0 < RPW; k0 += RB) {
-                                double2 v[RB][H];
-#pragma unroll
-                                for (int k = 0; k < RB; ++k) {
-                                    const int be = warp + NWA * (k0 + k);
-                                    const uint32_t B0 = pk<N>(g * z0 + be * w0, g * z1 + be * w1, g * z2 + be * w2);
-#pragma unroll
-                                    for (int h = 0; h < H; ++h) v[k][h] = __ldg(fc + swar_add(B0, Uh[h], H2));
-                                }
-#pragma unroll
-                                for (int k = 0; k < RB; ++k)
-                                    row_store_scan2<N, L>(v[k], warp + NWA * (k0 + k), raw, pre, tot, lane);
-                            }
+                for (int kp = 0; kp < NPL; ++kp) {
+                    const int g = rank + kp * kCL;
+                    cp_async_wait_all();
+                    role_sync(bar);  // plane g is in rawb[cur] (and the next record is visible)
+                    if (kp + 1 < NPL)
+                        gather_plane<N>(fc, rawb + (cur ^ 1) * Gm::PL, g + kCL, smA + 3, t, H2);
+                    else if (ndi >= 0)
+                        gather_plane<N>(fnext, rawb + (cur ^ 1) * Gm::PL, rank,
+                                        reinterpret_cast<const int *>(srec + (buf ^ 1) * kMaxRec) + 3, t, H2);
+                    const double2 *raw = rawb + cur * Gm::PL;
+                    // A2: in-row prefix sums, one thread per row (padded rows: conflict free)
+                    if (t < N && !(A.dbg & 16)) {
+                        const double2 *rr = raw + t * RS;
+                        double2 *pp = pre + t * RS;
+                        double2 acc = make_double2(0.0, 0.0);
+#pragma unroll 8
+                        for (int c = 0; c < N; ++c) {
+                            acc = add2(acc, rr[c]);
+                            pp[c] = acc;
+                            if (t < L) pp[N * RS + c] = acc;
                         }
-                        role_sync(bar);
-                        // A3: T by the sliding program (thread = column, β segment),
-                        // stored straight from registers (16 bytes per node)
-                        if (!(A.dbg & 4)) {
-                            const int al = tal;
-                            uint32_t x = pk<N>(g * z0 + al * u0 + tbe * w0, g * z1 + al * u1 + tbe * w1,
-                                               g * z2 + al * u2 + tbe * w2);
-                            double2 carry = make_double2(0.0, 0.0);
+                        tot[t] = acc;
+                        if (t < L) tot[t + N] = acc;
+                    }
+                    role_sync(bar);
+                    // A3: T by the sliding program (thread = column, β segment),
+                    // stored straight from registers (16 bytes per node)
+                    if (!(A.dbg & 4)) {
+                        const int al = tal;
+                        uint32_t x = pk<N>(g * z0 + al * u0 + tbe * w0, g * z1 + al * u1 + tbe * w1,
+                                           g * z2 + al * u2 + tbe * w2);
+                        double2 carry = make_double2(0.0, 0.0);
 #pragma unroll 1
-                            for (int c = 0; c < NCH; ++c) {
-                                const int be0 = tbe + c * L;
-                                double2 T[L + 1];
-                                if (c == 0) {
-                                    double2 acc = make_double2(0.0, 0.0);
-                                    for (int k = 0; k < ninit; ++k) {
-                                        const int4 en = sprog[k];
-                                        const int r0 = (be0 + en.x) & (N - 1);
-                                        const int b = al + en.z, a = al + en.y - 1;
-                                        double2 v = sub2(pre[r0 * N + (b & (N - 1))], pre[r0 * N + (a & (N - 1))]);
-                                        if ((b >> LOGN) != (a >> LOGN)) v = add2(v, tot[r0]);
-                                        acc = add2(acc, v);
-                                    }
-                                    T[0] = acc;
-                                } else {
-                                    T[0] = carry;
-                                }
-#pragma unroll
-                                for (int q = 1; q <= L; ++q) T[q] = make_double2(0.0, 0.0);
-                                for (int k = ninit; k < ninit + nstep; ++k) {
+                        for (int c = 0; c < NCH; ++c) {
+                            const int be0 = tbe + c * L;
+                            double2 T[L + 1];
+                            if (c == 0) {
+                                double2 acc = make_double2(0.0, 0.0);
+                                for (int k = 0; k < ninit; ++k) {
                                     const int4 en = sprog[k];
                                     const int r0 = (be0 + en.x) & (N - 1);
-                                    const double sgn = (double)en.w;
-                                    if (en.y == en.z) {
-                                        const double2 *q0 = raw + r0 * N + ((al + en.y) & (N - 1));
+                                    const int b = al + en.z, a = al + en.y - 1;
+                                    double2 v = sub2(pre[r0 * RS + (b & (N - 1))], pre[r0 * RS + (a & (N - 1))]);
+                                    if ((b >> LOGN) != (a >> LOGN)) v = add2(v, tot[r0]);
+                                    acc = add2(acc, v);
+                                }
+                                T[0] = acc;
+                            } else {
+                                T[0] = carry;
+                            }
 #pragma unroll
-                                        for (int q = 1; q <= L; ++q) T[q] = fma2(sgn, q0[(q - 1) * N], T[q]);
+                            for (int q = 1; q <= L; ++q) T[q] = make_double2(0.0, 0.0);
+                            for (int k = ninit; k < ninit + nstep; ++k) {
+                                const int4 en = sprog[k];
+                                const int r0 = (be0 + en.x) & (N - 1);
+                                const double sgn = (double)en.w;
+                                if (en.y == en.z) {
+                                    const double2 *q0 = raw + r0 * RS + ((al + en.y) & (N - 1));
+#pragma unroll
+                                    for (int q = 1; q <= L; ++q) T[q] = fma2(sgn, q0[(q - 1) * RS], T[q]);
+                                } else {
+                                    const int b = al + en.z, a = al + en.y - 1;
+                                    const double2 *qb = pre + r0 * RS + (b & (N - 1));
+                                    const double2 *qa = pre + r0 * RS + (a & (N - 1));
+                                    if ((b >> LOGN) != (a >> LOGN)) {
+                                        const double2 *qt = tot + r0;
+#pragma unroll
+                                        for (int q = 1; q <= L; ++q)
+                                            T[q] = fma2(sgn, add2(sub2(qb[(q - 1) * RS], qa[(q - 1) * RS]), qt[q - 1]), T[q]);
                                     } else {
-                                        const int b = al + en.z, a = al + en.y - 1;
-                                        const double2 *qb = pre + r0 * N + (b & (N - 1));
-                                        const double2 *qa = pre + r0 * N + (a & (N - 1));
-                                        if ((b >> LOGN) != (a >> LOGN)) {
-                                            const double2 *qt = tot + r0;
 #pragma unroll
-                                            for (int q = 1; q <= L; ++q)
-                                                T[q] = fma2(sgn, add2(sub2(qb[(q - 1) * N], qa[(q - 1) * N]), qt[q - 1]), T[q]);
-                                        } else {
-#pragma unroll
-                                            for (int q = 1; q <= L; ++q)
-                                                T[q] = fma2(sgn, sub2(qb[(q - 1) * N], qa[(q - 1) * N]), T[q]);
-                                        }
+                                        for (int q = 1; q <= L; ++q)
+                                            T[q] = fma2(sgn, sub2(qb[(q - 1) * RS], qa[(q - 1) * RS]), T[q]);
                                     }
                                 }
-#pragma unroll
-                                for (int q = 1; q <= L; ++q) T[q] = add2(T[q], T[q - 1]);
-#pragma unroll
-                                for (int q = 0; q < L; ++q) {
-                                    __stcg(Tb + x, T[q]);
-                                    x = swar_add(x, SW, H2);
-                                }
-                                carry = T[L];
                             }
+#pragma unroll
+                            for (int q = 1; q <= L; ++q) T[q] = add2(T[q], T[q - 1]);
+#pragma unroll
+                            for (int q = 0; q < L; ++q) {
+                                __stcg(Tb + x, T[q]);
+                                x = swar_add(x, SW, H2);
+                            }
+                            carry = T[L];
                         }
-                        role_sync(bar);  // raw/pre free for the next plane
                     }
+                    if (kp == 0 && ndi >= 0 && t < recw) srec[(buf ^ 1) * kMaxRec + t] = rnext;
+                    role_sync(bar);  // rawb[cur] and pre are free again
+                    cur ^= 1;
                 }
-                if (ndi >= 0 && t < recw) srec[(buf ^ 1) * kMaxRec + t] = rnext;
                 buf ^= 1;
                 role_signal(cA + rank, stepi + 1, leader, bar);
             } else {
