@@ -230,10 +230,10 @@ def run_ours(args):
     top_name, (top_ms, top_n) = top
     # algorithmic bytes per launch of the dominant kernel: the streaming
     # formulation charges (A+2)*8*N^3 bytes per cell-evaluation
-    # (one f pass per direction + f read + Q write).  k_cluster3d evaluates the
-    # whole batch (all cells, all directions) in one launch; the v1 orbit path
-    # launches k_rowsum once per direction chunk.
-    if top_name == "k_cluster3d":
+    # (one f pass per direction + f read + Q write).  k_gain3d evaluates the
+    # whole batch (all cells, all directions) in one launch per collide; the v1
+    # orbit path launches k_rowsum once per direction chunk.
+    if top_name == "k_gain3d":
         alg_bytes = (A + 2) * 8.0 * nodes * cells * psteps / top_n
     else:
         alg_bytes = (A + 2) * 8.0 * nodes * cells * psteps / max(1, prof.get("k_rowsum", (0, 1))[1])

@@ -126,7 +126,9 @@ def test_parity_full_2d(name):
 
 
 @pytest.mark.parametrize("d,N,Nbar,Nt", [(3, 16, 3, 3), (3, 16, 2, 7), (3, 8, 1, 3), (2, 32, 5, 7),
-                                         (2, 8, 1, 3), (2, 4, 1, 1)])
+                                         (2, 8, 1, 3), (2, 4, 1, 1),
+                                         # N = 32: the 3D frame-plane gain kernel + FFT loss, every node
+                                         (3, 32, 1, 3), (3, 32, 2, 4), (3, 32, 3, 3)])
 def test_parity_full_small(d, N, Nbar, Nt):
     f = dvm_inputs.two_bumps(d, N, 8.0, 1.5, 0.01, 3).reshape(-1)
     p = _plan(d, N, Nbar, Ntilde=Nt)
@@ -288,9 +290,9 @@ def test_batched_edge_cases():
 
 @pytest.mark.parametrize("d,N,Nbar,Nt,cells", [(3, 32, 4, 7, 1), (3, 64, 8, 14, 3), (3, 32, 3, 5, 40),
                                                (3, 64, 2, 5, 1), (3, 64, 1, 4, 2), (3, 32, 4, 7, 3)])
-def test_cluster_path_matches_orbit_path(d, N, Nbar, Nt, cells):
-    """The v2 cluster-per-cell kernel and the v1 orbit sweeps evaluate the same
-    operator (different summation orders): agreement to rounding."""
+def test_gain3d_path_matches_orbit_path(d, N, Nbar, Nt, cells):
+    """The 3D frame-plane gain kernel + FFT loss and the v1 orbit sweeps evaluate
+    the same operator (different summation orders): agreement to rounding."""
     f = np.random.default_rng(N + cells).uniform(0.0, 1.0, size=(cells, N ** d))
     p = _plan(d, N, Nbar, Ntilde=Nt)
     q2 = _gpu(p, f)
@@ -300,4 +302,21 @@ def test_cluster_path_matches_orbit_path(d, N, Nbar, Nt, cells):
     if N <= 64:
         pts = np.arange(0, N ** d, N ** d // 97)
         Qo, _, _ = oracle.collide(f[0], d, N, Nbar, Nt, 8.0, points=pts)
-        _assert_parity(q2[0][pts], Qo[0], f"cluster path N={N}", ref=np.abs(q1[0]).max())
+        _assert_parity(q2[0][pts], Qo[0], f"gain3d path N={N}", ref=np.abs(q1[0]).max())
+
+
+def test_gain3d_ragged_batches():
+    """Odd cell counts (the last cell pair is padded) and direction chunking for
+    small batches: every cell equals its single-cell evaluation to rounding and
+    matches the oracle on sampled nodes."""
+    N, Nbar, Nt = 32, 2, 5
+    f = np.random.default_rng(11).uniform(0.0, 1.0, size=(5, N ** 3))
+    p = _plan(3, N, Nbar, Ntilde=Nt)
+    for cells in (1, 3, 5):
+        qb = _gpu(p, f[:cells])
+        for c in range(cells):
+            q1 = _gpu(p, f[c]).reshape(-1)
+            np.testing.assert_allclose(qb[c], q1, rtol=0, atol=1e-13 * np.abs(q1).max())
+    pts = np.arange(0, N ** 3, 331)
+    Qo, _, _ = oracle.collide(f[4], 3, N, Nbar, Nt, 8.0, points=pts)
+    _assert_parity(qb[4][pts], Qo[0], "gain3d ragged batch")
