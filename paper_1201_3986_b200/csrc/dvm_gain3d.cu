@@ -443,7 +443,7 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_gain3d(GainArgs A)
                 const int z0 = smA[3], z1 = smA[4], z2 = smA[5];
                 const int u0 = smA[6], u1 = smA[7], u2 = smA[8];
                 const int w0 = smA[9], w1 = smA[10], w2 = smA[11];
-                const int ninit = smA[16], nstep = smA[17];
+                const int ninit = smA[16], nstep = smA[17], nraw = smA[19];
                 const uint32_t SW = pk<N>(w0, w1, w2);
                 const int tal = t & (N - 1);
                 const int tbe = (t >> LOGN) * SEGLEN;
@@ -454,25 +454,54 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_gain3d(GainArgs A)
                     const int g = rank + kp * kCL;
                     cp_async_wait_all();
                     role_sync(bar);  // plane g is in rawb[cur] (and the next record is visible)
-                    if (kp + 1 < NPL)
+                    if (A.dbg & 8) {
+                        // timing experiment: no gather (T on stale data)
+                    } else if (kp + 1 < NPL)
                         gather_plane<N>(fc, rawb + (cur ^ 1) * Gm::PL, g + kCL, smA + 3, t, H2);
                     else if (ndi >= 0)
                         gather_plane<N>(fnext, rawb + (cur ^ 1) * Gm::PL, rank,
                                         reinterpret_cast<const int *>(srec + (buf ^ 1) * kMaxRec) + 3, t, H2);
                     const double2 *raw = rawb + cur * Gm::PL;
-                    // A2: in-row prefix sums, one thread per row (padded rows: conflict free)
-                    if (t < N && !(A.dbg & 16)) {
-                        const double2 *rr = raw + t * RS;
-                        double2 *pp = pre + t * RS;
-                        double2 acc = make_double2(0.0, 0.0);
-#pragma unroll 8
-                        for (int c = 0; c < N; ++c) {
-                            acc = add2(acc, rr[c]);
-                            pp[c] = acc;
-                            if (t < L) pp[N * RS + c] = acc;
+                    // A2: in-row prefix sums.  Warp w scans rows 8w .. 8w+7 (N = 64) in four
+                    // 16-column quarters: lanes 8q + i take row 8w + i, quarter q, so each
+                    // quarter-warp reads 8 consecutive padded rows (conflict free); the
+                    // quarter totals are combined with shuffles across lanes i, i+8, ...
+                    if (!(A.dbg & 16)) {
+                        constexpr int QN = 32 / 8;          // quarters per row (lanes per row)
+                        constexpr int QL = N / QN;          // columns per quarter
+                        constexpr int RPWARP = 8;           // rows per warp
+                        for (int rb = warp * RPWARP; rb < N; rb += (kRoleT / 32) * RPWARP) {
+                            const int row = rb + (lane & 7), qd = lane >> 3;
+                            const double2 *rr = raw + row * RS + qd * QL;
+                            double2 v[QL];
+#pragma unroll
+                            for (int c = 0; c < QL; ++c) v[c] = rr[c];
+#pragma unroll
+                            for (int c = 1; c < QL; ++c) v[c] = add2(v[c], v[c - 1]);
+                            // exclusive prefix of the quarter totals over qd = 0..3 (lanes i + 8 qd)
+                            double2 x = v[QL - 1];
+#pragma unroll
+                            for (int o = 8; o < 32; o <<= 1) {
+                                const double yx = __shfl_up_sync(0xffffffffu, x.x, o);
+                                const double yy = __shfl_up_sync(0xffffffffu, x.y, o);
+                                if (lane >= o) {
+                                    x.x += yx;
+                                    x.y += yy;
+                                }
+                            }
+                            const double2 excl = sub2(x, v[QL - 1]);
+                            double2 *pp = pre + row * RS + qd * QL;
+#pragma unroll
+                            for (int c = 0; c < QL; ++c) {
+                                const double2 o2 = add2(v[c], excl);
+                                pp[c] = o2;
+                                if (row < L) pp[N * RS + c] = o2;
+                            }
+                            if (qd == QN - 1) {
+                                tot[row] = x;
+                                if (row < L) tot[row + N] = x;
+                            }
                         }
-                        tot[t] = acc;
-                        if (t < L) tot[t + N] = acc;
                     }
                     role_sync(bar);
                     // A3: T by the sliding program (thread = column, β segment),
@@ -502,28 +531,31 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_gain3d(GainArgs A)
                             }
 #pragma unroll
                             for (int q = 1; q <= L; ++q) T[q] = make_double2(0.0, 0.0);
-                            for (int k = ninit; k < ninit + nstep; ++k) {
+                            // single-node entries (host-sorted first), then row ranges
+#pragma unroll 2
+                            for (int k = ninit; k < ninit + nraw; ++k) {
                                 const int4 en = sprog[k];
                                 const int r0 = (be0 + en.x) & (N - 1);
                                 const double sgn = (double)en.w;
-                                if (en.y == en.z) {
-                                    const double2 *q0 = raw + r0 * RS + ((al + en.y) & (N - 1));
+                                const double2 *q0 = raw + r0 * RS + ((al + en.y) & (N - 1));
 #pragma unroll
-                                    for (int q = 1; q <= L; ++q) T[q] = fma2(sgn, q0[(q - 1) * RS], T[q]);
-                                } else {
-                                    const int b = al + en.z, a = al + en.y - 1;
-                                    const double2 *qb = pre + r0 * RS + (b & (N - 1));
-                                    const double2 *qa = pre + r0 * RS + (a & (N - 1));
-                                    if ((b >> LOGN) != (a >> LOGN)) {
-                                        const double2 *qt = tot + r0;
+                                for (int q = 1; q <= L; ++q) T[q] = fma2(sgn, q0[(q - 1) * RS], T[q]);
+                            }
+#pragma unroll 2
+                            for (int k = ninit + nraw; k < ninit + nstep; ++k) {
+                                const int4 en = sprog[k];
+                                const int r0 = (be0 + en.x) & (N - 1);
+                                const double sgn = (double)en.w;
+                                const int b = al + en.z, a = al + en.y - 1;
+                                const double2 *qb = pre + r0 * RS + (b & (N - 1));
+                                const double2 *qa = pre + r0 * RS + (a & (N - 1));
+                                const double2 *qt = tot + r0;
+                                const double wr = (b >> LOGN) != (a >> LOGN) ? 1.0 : 0.0;  // periodic wrap
 #pragma unroll
-                                        for (int q = 1; q <= L; ++q)
-                                            T[q] = fma2(sgn, add2(sub2(qb[(q - 1) * RS], qa[(q - 1) * RS]), qt[q - 1]), T[q]);
-                                    } else {
-#pragma unroll
-                                        for (int q = 1; q <= L; ++q)
-                                            T[q] = fma2(sgn, sub2(qb[(q - 1) * RS], qa[(q - 1) * RS]), T[q]);
-                                    }
+                                for (int q = 1; q <= L; ++q) {
+                                    const double2 d = sub2(qb[(q - 1) * RS], qa[(q - 1) * RS]);
+                                    const double2 tq = qt[q - 1];
+                                    T[q] = fma2(sgn, make_double2(fma(wr, tq.x, d.x), fma(wr, tq.y, d.y)), T[q]);
                                 }
                             }
 #pragma unroll
@@ -874,11 +906,18 @@ dvm_status_t build_gain3d(dvm_plan_s *P)
         m[15] = F.M;
         m[16] = (int)F.init.size();
         m[17] = (int)F.step.size();
+        int nraw = 0;
+        for (const auto &x : F.step) nraw += x.t1 == x.t2;
+        m[19] = nraw;
         int4 *r = &rec[(size_t)k * recw];
         for (int q = 0; q < 6; ++q) r[q] = make_int4(m[4 * q], m[4 * q + 1], m[4 * q + 2], m[4 * q + 3]);
         int q = 6;
         for (const auto &x : F.init) r[q++] = make_int4(x.rho, x.t1, x.t2, x.sign);
-        for (const auto &x : F.step) r[q++] = make_int4(x.rho, x.t1, x.t2, x.sign);
+        // step entries: single nodes first, then row ranges (two branch-free loops)
+        for (const auto &x : F.step)
+            if (x.t1 == x.t2) r[q++] = make_int4(x.rho, x.t1, x.t2, x.sign);
+        for (const auto &x : F.step)
+            if (x.t1 != x.t2) r[q++] = make_int4(x.rho, x.t1, x.t2, x.sign);
     }
     GainTables &g = P->g;
     g.recw = recw;
