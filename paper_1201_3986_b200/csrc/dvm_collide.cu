@@ -313,9 +313,10 @@ dvm_status_t collide_batched(dvm_plan_s *P, const double *f, double *Q, int64_t 
 {
     const Geo g = geo_of(P);
     if (ncells == 0) return DVM_OK;
-    if (P->d == 3 && !P->force_v1) {
+    if (!P->force_v1) {
         bool handled = false;
-        dvm_status_t st = collide_gain3d(P, f, stride, Q, stride, ncells, &handled);
+        dvm_status_t st = P->d == 3 ? collide_gain3d(P, f, stride, Q, stride, ncells, &handled)
+                                    : collide_pair2d(P, f, stride, Q, stride, ncells, &handled);
         if (st || handled) return st;
     }
     const int zero_blocks = 592;
@@ -412,7 +413,7 @@ void free_workspace(dvm_plan_s *P)
 {
     clear_profile(P);
     Workspace &w = P->ws;
-    void *ptrs[] = {w.S, w.part, w.f_stage, w.q_stage, w.mom_partial, w.mom_dev, w.qtmp, w.fft_z, w.g3_f, w.g3_t, w.g3_q, w.g3_ctr};
+    void *ptrs[] = {w.S, w.part, w.f_stage, w.q_stage, w.mom_partial, w.mom_dev, w.qtmp, w.fft_z, w.g3_f, w.g3_t, w.g3_q, w.g3_ctr, w.p2_scr, w.p2_part};
     for (void *q : ptrs)
         if (q) cudaFree(q);
     w = Workspace{};

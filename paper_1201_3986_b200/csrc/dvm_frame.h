@@ -293,12 +293,11 @@ inline bool build_dir(const int *e, int Nt, int N, int seg_len, DirFrame &out)
                 u[j] = m[0] * v1[j] + m[1] * v2[j];
                 w[j] = m[2] * v1[j] + m[3] * v2[j];
             }
-            long long wn[3] = {-w[0], -w[1], -w[2]}, un[3] = {-u[0], -u[1], -u[2]};
+            long long un[3] = {-u[0], -u[1], -u[2]};
             consider(u, w);    // slide along +w
             consider(w, u);    // rows along w, slide along u
             consider(un, w);
             consider(w, un);
-            (void)wn;
         }
     }
     if (!have) return false;

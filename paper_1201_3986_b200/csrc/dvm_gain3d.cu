@@ -37,169 +37,6 @@ namespace {
 constexpr int kCL = 16;         // CTAs per cell group
 constexpr int kMaxRec = 72;     // int4 words of a direction record (6 meta + program entries)
 constexpr int kMaxMS = 32;      // line half-width M_e held in shared memory
-constexpr int kFT = 256;        // FFT threads per CTA
-
-// ------------------------------------------------------------------ FFT
-struct FftArgs {
-    int d, ax, inverse;
-    int64_t npairs;
-    // real input (first forward pass): cells 2p, 2p+1 of r0 (cell stride r_stride, r_cells cells)
-    const double *r0;
-    int64_t r_stride, r_cells, r_first;  // r_first: index of the batch's first cell
-    const double2 *zin;
-    double2 *zout;
-    const double *mult;  // optional real multiplier per node (λ̂)
-    // epilogue (last inverse pass): Q[c] = -f[c] * Λ[c]
-    double *q;
-    int64_t q_stride;
-    double2 *qI;  // epilogue, interleaved mode: qI[pair][node] = (-f_{2p} Λ_{2p}, -f_{2p+1} Λ_{2p+1})
-    const double *f;
-    int64_t f_stride;
-    double scale;
-    const double2 *tw;  // exp(-2πik/N), k < N/2
-};
-
-__device__ __forceinline__ double2 cmul(double2 a, double2 b)
-{
-    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
-}
-
-// One radix-2 FFT pass of length N along axis `ax` for every line of every
-// pair in the batch.  Tile = B lines (contiguous rows for the last axis,
-// lines adjacent in the last axis otherwise).
-template <int N>
-__global__ void __launch_bounds__(kFT) k_fft_pass(FftArgs A)
-{
-    constexpr int B = (1024 / N) < N ? (1024 / N) : N;
-    constexpr int LOGN = N == 16 ? 4 : N == 32 ? 5 : N == 64 ? 6 : N == 128 ? 7 : 8;
-    __shared__ double2 buf[B * N];
-    const int d = A.d, ax = A.ax;
-    int64_t nodes = 1;
-    for (int j = 0; j < d; ++j) nodes *= N;
-    const int64_t lines = nodes / N;
-    const int64_t tiles_per_pair = lines / B;
-    const int64_t tile_all = blockIdx.x;
-    const int64_t pair = tile_all / tiles_per_pair;
-    const int64_t tile = tile_all % tiles_per_pair;
-    if (pair >= A.npairs) return;
-    const bool last_axis = ax == d - 1;
-    int64_t sax = 1;
-    for (int j = ax + 1; j < d; ++j) sax *= N;
-    // address of element t of line i of this tile (within the pair's cell)
-    auto addr = [&](int i, int t) -> int64_t {
-        if (last_axis) return (tile * B + i) * N + t;
-        const int64_t x_last0 = (tile % (N / B)) * B;
-        const int64_t outer = tile / (N / B);  // the remaining coordinate (d = 3) or 0
-        int64_t o = 0;
-        if (d == 3) o = ax == 0 ? outer * N : outer * (int64_t)N * N;
-        return o + (int64_t)t * sax + x_last0 + i;
-    };
-    // load (bit-reversed)
-    for (int idx = threadIdx.x; idx < B * N; idx += kFT) {
-        int i, t;
-        if (last_axis) { i = idx / N; t = idx % N; }
-        else { i = idx % B; t = idx / B; }
-        const int64_t a = addr(i, t);
-        double2 v;
-        if (A.r0) {
-            const int64_t c0 = A.r_first + 2 * pair, c1 = c0 + 1;
-            v.x = A.r0[c0 * A.r_stride + a];
-            v.y = c1 < A.r_cells ? A.r0[c1 * A.r_stride + a] : 0.0;
-        } else {
-            v = A.zin[pair * nodes + a];
-        }
-        const int tr = (int)(__brev((unsigned)t) >> (32 - LOGN));
-        buf[i * N + tr] = v;
-    }
-    __syncthreads();
-    for (int half = 1; half < N; half <<= 1) {
-        for (int b = threadIdx.x; b < B * N / 2; b += kFT) {
-            const int i = b / (N / 2), k = b % (N / 2);
-            const int pos = k & (half - 1), grp = k / half;
-            const int i0 = grp * 2 * half + pos, i1 = i0 + half;
-            double2 w = A.tw[pos * (N / (2 * half))];
-            if (A.inverse) w.y = -w.y;
-            const double2 u = buf[i * N + i0], v = cmul(buf[i * N + i1], w);
-            buf[i * N + i0] = make_double2(u.x + v.x, u.y + v.y);
-            buf[i * N + i1] = make_double2(u.x - v.x, u.y - v.y);
-        }
-        __syncthreads();
-    }
-    for (int idx = threadIdx.x; idx < B * N; idx += kFT) {
-        int i, t;
-        if (last_axis) { i = idx / N; t = idx % N; }
-        else { i = idx % B; t = idx / B; }
-        const int64_t a = addr(i, t);
-        double2 v = buf[i * N + t];
-        if (A.mult) {
-            const double m = A.mult[a];
-            v.x *= m;
-            v.y *= m;
-        }
-        if (A.qI) {
-            const int64_t c0 = A.r_first + 2 * pair, c1 = c0 + 1;
-            double2 o;
-            o.x = -A.f[c0 * A.f_stride + a] * (v.x * A.scale);
-            o.y = c1 < A.r_cells ? -A.f[c1 * A.f_stride + a] * (v.y * A.scale) : 0.0;
-            A.qI[(A.r_first / 2 + pair) * nodes + a] = o;
-        } else if (A.q) {
-            const int64_t c0 = A.r_first + 2 * pair, c1 = c0 + 1;
-            A.q[c0 * A.q_stride + a] = -A.f[c0 * A.f_stride + a] * (v.x * A.scale);
-            if (c1 < A.r_cells) A.q[c1 * A.q_stride + a] = -A.f[c1 * A.f_stride + a] * (v.y * A.scale);
-        } else {
-            A.zout[pair * nodes + a] = v;
-        }
-    }
-}
-
-__global__ void k_twiddles(int N, double2 *tw)
-{
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= N / 2) return;
-    double s, c;
-    sincospi(2.0 * k / N, &s, &c);
-    tw[k] = make_double2(c, -s);
-}
-
-// λ(j) = Σ_e a_e #{(m, l): 1 <= |m| <= M_e, l ∈ e^⊥ ∩ [-Ñ,Ñ]^3, me + l ≡ j},
-// one thread per node j, directions in local-list order (deterministic).
-__global__ void k_lambda(int N, int p, int Nt, const int *local, int nloc, const int *E, const int *M,
-                         const double *aw, double *lam)
-{
-    const int64_t nodes = (int64_t)N * N * N;
-    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= nodes) return;
-    const int jc[3] = {(int)(j >> (2 * p)), (int)((j >> p) & (N - 1)), (int)(j & (N - 1))};
-    double acc = 0.0;
-    for (int k = 0; k < nloc; ++k) {
-        const int di = local[k];
-        const int e0 = E[3 * di], e1 = E[3 * di + 1], e2 = E[3 * di + 2];
-        const int m_e = M[di];
-        int cnt = 0;
-        for (int m = 1; m <= m_e; ++m)
-            for (int s = -1; s <= 1; s += 2) {
-                int l[3];
-                const int ee[3] = {e0, e1, e2};
-                bool ok = true;
-                for (int q = 0; q < 3; ++q) {
-                    int v = (jc[q] - s * m * ee[q]) % N;
-                    if (v < 0) v += N;
-                    if (v > N / 2) v -= N;  // centred representative (|l| <= Ñ < N/2)
-                    l[q] = v;
-                    if (v > Nt || v < -Nt) ok = false;
-                }
-                if (ok && l[0] * e0 + l[1] * e1 + l[2] * e2 == 0) ++cnt;
-            }
-        if (cnt) acc += aw[di] * cnt;
-    }
-    lam[j] = acc;
-}
-
-__global__ void k_take_real(const double2 *z, int64_t n, double *out)
-{
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        out[i] = z[i].x;
-}
 
 // ------------------------------------------------------------------ gain
 struct GainArgs {
@@ -350,11 +187,9 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_gain3d(GainArgs A)
     using Gm = G3Geom<N>;
     constexpr int LOGN = Gm::LOGN;
     constexpr int64_t NODES = (int64_t)N * N * N;
-    constexpr int SEGS = Gm::SEGS;
     constexpr int SEGLEN = Gm::SEGLEN;
     constexpr int L = Gm::L;
     constexpr int NCH = Gm::NCH;
-    constexpr int H = N / 32;
     constexpr int NPR = (int)(NODES / kCL);  // phase-B nodes per CTA
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int RS = Gm::RS;
@@ -696,95 +531,6 @@ __global__ void k_deinterleave(const double2 *__restrict__ QI, int nchunks, int6
 size_t gain_smem_bytes(int N) { return N == 32 ? G3Geom<32>::smem : G3Geom<64>::smem; }
 
 
-template <typename T>
-dvm_status_t grow(T **ptr, size_t *cap, size_t need, cudaStream_t s)
-{
-    if (*cap >= need) return DVM_OK;
-    DVM_CUDA(cudaStreamSynchronize(s));
-    if (*ptr) cudaFree(*ptr);
-    *ptr = nullptr;
-    *cap = 0;
-    if (cudaMalloc(ptr, sizeof(T) * need) != cudaSuccess) {
-        *ptr = nullptr;
-        cudaGetLastError();
-        set_error("gain3d workspace allocation failed");
-        return DVM_E_NOMEM;
-    }
-    *cap = need;
-    return DVM_OK;
-}
-
-template <int N>
-dvm_status_t fft_pass(dvm_plan_s *P, const FftArgs &a)
-{
-    constexpr int B = (1024 / N) < N ? (1024 / N) : N;
-    int64_t nodes = 1;
-    for (int j = 0; j < a.d; ++j) nodes *= N;
-    const int64_t tiles = a.npairs * (nodes / N / B);
-    LaunchScope ls(P, KC_FFT);
-    k_fft_pass<N><<<(unsigned)tiles, kFT, 0, P->stream>>>(a);
-    DVM_CUDA(cudaGetLastError());
-    return DVM_OK;
-}
-
-dvm_status_t fft_dispatch(dvm_plan_s *P, const FftArgs &a)
-{
-    switch (P->N) {
-    case 16: return fft_pass<16>(P, a);
-    case 32: return fft_pass<32>(P, a);
-    case 64: return fft_pass<64>(P, a);
-    case 128: return fft_pass<128>(P, a);
-    case 256: return fft_pass<256>(P, a);
-    default: set_error("FFT length unsupported"); return DVM_E_UNSUPPORTED;
-    }
-}
-
-// Loss initialisation Q[c] := −f[c] Λ[c] for cells [0, ncells) (Λ = λ ⊛ f).
-dvm_status_t loss_init(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q, int64_t q_stride, int64_t ncells,
-                       double2 *QI = nullptr)
-{
-    const int d = P->d;
-    int64_t nodes = 1;
-    for (int j = 0; j < d; ++j) nodes *= P->N;
-    const int64_t npairs_all = (ncells + 1) / 2;
-    const int64_t batch = std::max<int64_t>(1, std::min<int64_t>(npairs_all, (int64_t)((256ull << 20) / (16 * nodes))));
-    Workspace &w = P->ws;
-    dvm_status_t st;
-    if ((st = grow(&w.fft_z, &w.fft_z_elems, (size_t)(batch * nodes), P->stream))) return st;
-    double scale = 1.0 / (double)nodes;
-    for (int64_t p0 = 0; p0 < npairs_all; p0 += batch) {
-        const int64_t np = std::min(batch, npairs_all - p0);
-        for (int k = 0; k < 2 * d; ++k) {
-            FftArgs a = {};
-            a.d = d;
-            a.npairs = np;
-            a.tw = P->g.tw;
-            a.r_cells = ncells;
-            a.r_first = 2 * p0;
-            const bool fwd = k < d;
-            a.inverse = fwd ? 0 : 1;
-            a.ax = fwd ? d - 1 - k : k - d;
-            a.zin = w.fft_z;
-            a.zout = w.fft_z;
-            if (k == 0) {
-                a.r0 = f;
-                a.r_stride = f_stride;
-            }
-            if (k == d - 1) a.mult = P->g.lamhat;
-            if (k == 2 * d - 1) {
-                a.qI = QI;
-                a.q = Q;
-                a.q_stride = q_stride;
-                a.f = f;
-                a.f_stride = f_stride;
-                a.scale = scale;
-            }
-            if ((st = fft_dispatch(P, a))) return st;
-        }
-    }
-    return DVM_OK;
-}
-
 template <int N>
 dvm_status_t launch_gain(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q, int64_t q_stride,
                          int64_t ncells)
@@ -923,54 +669,11 @@ dvm_status_t build_gain3d(dvm_plan_s *P)
     g.recw = recw;
     DVM_CUDA(cudaMalloc(&g.rec, sizeof(int4) * rec.size()));
     DVM_CUDA(cudaMalloc(&g.aw, sizeof(double) * aw.size()));
-    DVM_CUDA(cudaMalloc(&g.tw, sizeof(double2) * N / 2));
-    const int64_t nodes = (int64_t)N * N * N;
-    DVM_CUDA(cudaMalloc(&g.lamhat, sizeof(double) * nodes));
-    g.bytes = sizeof(int4) * rec.size() + sizeof(double) * aw.size() + sizeof(double2) * N / 2 +
-              sizeof(double) * nodes;
+    g.bytes = sizeof(int4) * rec.size() + sizeof(double) * aw.size();
     DVM_CUDA(cudaMemcpyAsync(g.rec, rec.data(), sizeof(int4) * rec.size(), cudaMemcpyHostToDevice, P->stream));
     DVM_CUDA(cudaMemcpyAsync(g.aw, aw.data(), sizeof(double) * aw.size(), cudaMemcpyHostToDevice, P->stream));
-    {
-        LaunchScope ls(P, KC_PLAN);
-        k_twiddles<<<1, 128, 0, P->stream>>>(N, g.tw);
-    }
-    // λ on the grid, then λ̂ = FFT(λ) (real: λ is even)
-    double *lam = nullptr;
-    double2 *z = nullptr;
-    DVM_CUDA(cudaMalloc(&lam, sizeof(double) * nodes));
-    DVM_CUDA(cudaMalloc(&z, sizeof(double2) * nodes));
-    {
-        LaunchScope ls(P, KC_PLAN);
-        k_lambda<<<(unsigned)((nodes + 127) / 128), 128, 0, P->stream>>>(N, P->p, P->Ntilde, P->t.local, nloc,
-                                                                         P->t.e, P->t.M, P->t.a, lam);
-    }
-    DVM_CUDA(cudaGetLastError());
-    dvm_status_t st = DVM_OK;
-    for (int k = 0; k < 3 && !st; ++k) {
-        FftArgs a = {};
-        a.d = 3;
-        a.npairs = 1;
-        a.tw = g.tw;
-        a.r_cells = 1;
-        a.r_first = 0;
-        a.ax = 2 - k;
-        a.zin = z;
-        a.zout = z;
-        if (k == 0) {
-            a.r0 = lam;
-            a.r_stride = nodes;
-        }
-        st = fft_dispatch(P, a);
-    }
-    if (!st) {
-        LaunchScope ls(P, KC_PLAN);
-        k_take_real<<<256, 256, 0, P->stream>>>(z, nodes, g.lamhat);
-    }
-    cudaStreamSynchronize(P->stream);
-    cudaFree(lam);
-    cudaFree(z);
+    const dvm_status_t st = build_loss(P);
     if (st) return st;
-    DVM_CUDA(cudaGetLastError());
     g.ready = true;
     return DVM_OK;
 }
@@ -978,7 +681,7 @@ dvm_status_t build_gain3d(dvm_plan_s *P)
 void free_gain3d(dvm_plan_s *P)
 {
     GainTables &g = P->g;
-    void *ptrs[] = {g.rec, g.aw, g.tw, g.lamhat};
+    void *ptrs[] = {g.rec, g.aw, g.tw, g.lamhat, g.units};
     for (void *q : ptrs)
         if (q) cudaFree(q);
     g = GainTables{};

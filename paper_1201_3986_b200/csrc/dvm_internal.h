@@ -75,6 +75,9 @@ struct Workspace {
     double2 *g3_q = nullptr;        // 3D gain: interleaved Q accumulators [chunks][pairs][nodes]
     unsigned int *g3_ctr = nullptr; // 3D gain: group barrier counters
     size_t fft_z_elems = 0, g3_f_elems = 0, g3_t_elems = 0, g3_q_elems = 0, g3_ctr_elems = 0;
+    double *p2_scr = nullptr;       // 2D pair path: line windows of the first direction [units][cells][nodes]
+    double *p2_part = nullptr;      // 2D pair path: partial gains [units][cells][nodes]
+    size_t p2_scr_elems = 0, p2_part_elems = 0;
 };
 
 }  // namespace dvm
@@ -95,7 +98,9 @@ struct GainTables {
     int recw = 0;
     double *aw = nullptr;     // [A_local] a_e
     double2 *tw = nullptr;    // FFT twiddles exp(-2πik/N), k < N/2
-    double *lamhat = nullptr; // [N^3] spectrum of the loss kernel λ (real)
+    double *lamhat = nullptr; // [N^d] spectrum of the loss kernel λ (real)
+    void *units = nullptr;    // 2D: direction-pair units (dvm_pair2d.cu)
+    int nunits = 0;
     size_t bytes = 0;
 };
 }  // namespace dvm
@@ -151,6 +156,8 @@ struct LaunchScope {
 };
 void clear_profile(dvm_plan_s *P);
 
+
+
 // error reporting (thread-local message)
 void set_error(const std::string &msg);
 dvm_status_t cuda_fail(cudaError_t err, const char *what);
@@ -160,6 +167,26 @@ dvm_status_t cuda_fail(cudaError_t err, const char *what);
         cudaError_t _e = (call);                                         \
         if (_e != cudaSuccess) return ::dvm::cuda_fail(_e, #call);       \
     } while (0)
+
+// Grow-only device workspace buffer (stream-synchronised before a reallocation).
+template <typename T>
+dvm_status_t grow(T **ptr, size_t *cap, size_t need, cudaStream_t s)
+{
+    if (*cap >= need) return DVM_OK;
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+    if (*ptr) cudaFree(*ptr);
+    *ptr = nullptr;
+    *cap = 0;
+    if (cudaMalloc(ptr, sizeof(T) * need) != cudaSuccess) {
+        *ptr = nullptr;
+        cudaGetLastError();
+        set_error("workspace allocation failed");
+        return DVM_E_NOMEM;
+    }
+    *cap = need;
+    return DVM_OK;
+}
 
 // plan construction (dvm_plan.cu)
 dvm_status_t build_table(dvm_plan_s *P);
@@ -172,7 +199,14 @@ dvm_status_t axpy(dvm_plan_s *P, double *f, const double *q, double dt);
 dvm_status_t zero_cells(dvm_plan_s *P, double *Q, int64_t q_stride, int64_t ncells, int64_t nodes);
 dvm_status_t reduce_slots(dvm_plan_s *P, double *Q, int64_t q_stride, const double *part, int64_t slot_elems,
                           int nslots, int64_t ncells, int64_t nodes);
+// 3D gain (dvm_gain3d.cu), loss as one FFT convolution (dvm_loss.cu)
+dvm_status_t build_loss(dvm_plan_s *P);
+dvm_status_t loss_init(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q, int64_t q_stride, int64_t ncells,
+                       double2 *QI);
 dvm_status_t build_gain3d(dvm_plan_s *P);
+dvm_status_t build_pair2d(dvm_plan_s *P);
+dvm_status_t collide_pair2d(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q, int64_t q_stride,
+                            int64_t ncells, bool *handled);
 void free_gain3d(dvm_plan_s *P);
 dvm_status_t collide_gain3d(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q, int64_t q_stride,
                             int64_t ncells, bool *handled);

@@ -1,0 +1,320 @@
+// dvm_loss.cu -- the loss term of Q = D^{Ñ,N̄}(f,f) as one periodic convolution
+// (reading R21): Σ_e a_e f U_e = f Λ, Λ = λ ⊛ f with the fixed kernel
+//   λ(j) = Σ_e a_e #{(m, l) : 1 <= |m| <= M_e, l ∈ P_e, me + l ≡ j (mod N)}
+// (β̃ = β − β(L,L); the paper evaluates this convolution
+// spectrally).  λ is even, so λ̂ is real and two real cells
+// share one complex transform (f_{2p} + i f_{2p+1}).
+//
+//   plan time   k_lambda (one thread per node, directions in order) and
+//               λ̂ = FFT(λ) with the passes below (k_take_real)
+//   per collide loss_init: d forward passes (the first reads f, the last
+//               multiplies by λ̂), d inverse passes (the last writes −f Λ)
+// k_fft_pass is a radix-2 fp64 pass along one axis over tiles of lines in
+// shared memory, twiddles exp(−2πik/N) from sincospi.
+#include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
+
+#include <algorithm>
+
+#include "dvm_internal.h"
+
+namespace dvm {
+namespace {
+
+constexpr int kFT = 256;  // FFT threads per CTA
+
+struct FftArgs {
+    int d, ax, inverse;
+    int64_t npairs;
+    // real input (first forward pass): cells 2p, 2p+1 of r0 (cell stride r_stride, r_cells cells)
+    const double *r0;
+    int64_t r_stride, r_cells, r_first;  // r_first: index of the batch's first cell
+    const double2 *zin;
+    double2 *zout;
+    const double *mult;  // optional real multiplier per node (λ̂)
+    // epilogue (last inverse pass): Q[c] = -f[c] * Λ[c]
+    double *q;
+    int64_t q_stride;
+    double2 *qI;  // epilogue, interleaved mode: qI[pair][node] = (-f_{2p} Λ_{2p}, -f_{2p+1} Λ_{2p+1})
+    const double *f;
+    int64_t f_stride;
+    double scale;
+    const double2 *tw;  // exp(-2πik/N), k < N/2
+};
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b)
+{
+    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+// One radix-2 FFT pass of length N along axis `ax` for every line of every
+// pair in the batch.  Tile = B lines (contiguous rows for the last axis,
+// lines adjacent in the last axis otherwise).
+template <int N>
+__global__ void __launch_bounds__(kFT) k_fft_pass(FftArgs A)
+{
+    constexpr int B = (1024 / N) < N ? (1024 / N) : N;
+    constexpr int LOGN = N == 16 ? 4 : N == 32 ? 5 : N == 64 ? 6 : N == 128 ? 7 : 8;
+    __shared__ double2 buf[B * N];
+    const int d = A.d, ax = A.ax;
+    int64_t nodes = 1;
+    for (int j = 0; j < d; ++j) nodes *= N;
+    const int64_t lines = nodes / N;
+    const int64_t tiles_per_pair = lines / B;
+    const int64_t tile_all = blockIdx.x;
+    const int64_t pair = tile_all / tiles_per_pair;
+    const int64_t tile = tile_all % tiles_per_pair;
+    if (pair >= A.npairs) return;
+    const bool last_axis = ax == d - 1;
+    int64_t sax = 1;
+    for (int j = ax + 1; j < d; ++j) sax *= N;
+    // address of element t of line i of this tile (within the pair's cell)
+    auto addr = [&](int i, int t) -> int64_t {
+        if (last_axis) return (tile * B + i) * N + t;
+        const int64_t x_last0 = (tile % (N / B)) * B;
+        const int64_t outer = tile / (N / B);  // the remaining coordinate (d = 3) or 0
+        int64_t o = 0;
+        if (d == 3) o = ax == 0 ? outer * N : outer * (int64_t)N * N;
+        return o + (int64_t)t * sax + x_last0 + i;
+    };
+    // load (bit-reversed)
+    for (int idx = threadIdx.x; idx < B * N; idx += kFT) {
+        int i, t;
+        if (last_axis) { i = idx / N; t = idx % N; }
+        else { i = idx % B; t = idx / B; }
+        const int64_t a = addr(i, t);
+        double2 v;
+        if (A.r0) {
+            const int64_t c0 = A.r_first + 2 * pair, c1 = c0 + 1;
+            v.x = A.r0[c0 * A.r_stride + a];
+            v.y = c1 < A.r_cells ? A.r0[c1 * A.r_stride + a] : 0.0;
+        } else {
+            v = A.zin[pair * nodes + a];
+        }
+        const int tr = (int)(__brev((unsigned)t) >> (32 - LOGN));
+        buf[i * N + tr] = v;
+    }
+    __syncthreads();
+    for (int half = 1; half < N; half <<= 1) {
+        for (int b = threadIdx.x; b < B * N / 2; b += kFT) {
+            const int i = b / (N / 2), k = b % (N / 2);
+            const int pos = k & (half - 1), grp = k / half;
+            const int i0 = grp * 2 * half + pos, i1 = i0 + half;
+            double2 w = A.tw[pos * (N / (2 * half))];
+            if (A.inverse) w.y = -w.y;
+            const double2 u = buf[i * N + i0], v = cmul(buf[i * N + i1], w);
+            buf[i * N + i0] = make_double2(u.x + v.x, u.y + v.y);
+            buf[i * N + i1] = make_double2(u.x - v.x, u.y - v.y);
+        }
+        __syncthreads();
+    }
+    for (int idx = threadIdx.x; idx < B * N; idx += kFT) {
+        int i, t;
+        if (last_axis) { i = idx / N; t = idx % N; }
+        else { i = idx % B; t = idx / B; }
+        const int64_t a = addr(i, t);
+        double2 v = buf[i * N + t];
+        if (A.mult) {
+            const double m = A.mult[a];
+            v.x *= m;
+            v.y *= m;
+        }
+        if (A.qI) {
+            const int64_t c0 = A.r_first + 2 * pair, c1 = c0 + 1;
+            double2 o;
+            o.x = -A.f[c0 * A.f_stride + a] * (v.x * A.scale);
+            o.y = c1 < A.r_cells ? -A.f[c1 * A.f_stride + a] * (v.y * A.scale) : 0.0;
+            A.qI[(A.r_first / 2 + pair) * nodes + a] = o;
+        } else if (A.q) {
+            const int64_t c0 = A.r_first + 2 * pair, c1 = c0 + 1;
+            A.q[c0 * A.q_stride + a] = -A.f[c0 * A.f_stride + a] * (v.x * A.scale);
+            if (c1 < A.r_cells) A.q[c1 * A.q_stride + a] = -A.f[c1 * A.f_stride + a] * (v.y * A.scale);
+        } else {
+            A.zout[pair * nodes + a] = v;
+        }
+    }
+}
+
+__global__ void k_twiddles(int N, double2 *tw)
+{
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= N / 2) return;
+    double s, c;
+    sincospi(2.0 * k / N, &s, &c);
+    tw[k] = make_double2(c, -s);
+}
+
+// λ(j) = Σ_e a_e #{(m, l): 1 <= |m| <= M_e, l ∈ e^⊥ ∩ [-Ñ,Ñ]^d, me + l ≡ j},
+// one thread per node j, directions in local-list order (deterministic).
+// (2D: e^⊥ ∩ box = {n e^⊥ : |n| <= M_e}, the perp line of PAPER.md:803, 818.)
+__global__ void k_lambda(int d, int N, int p, int Nt, const int *local, int nloc, const int *E, const int *M,
+                         const double *aw, double *lam)
+{
+    int64_t nodes = 1;
+    for (int q = 0; q < d; ++q) nodes *= N;
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= nodes) return;
+    int jc[3] = {0, 0, 0};
+    for (int q = d - 1, sh = 0; q >= 0; --q, sh += p) jc[q] = (int)((j >> sh) & (N - 1));
+    double acc = 0.0;
+    for (int k = 0; k < nloc; ++k) {
+        const int di = local[k];
+        const int ee[3] = {E[3 * di], E[3 * di + 1], E[3 * di + 2]};
+        const int m_e = M[di];
+        int cnt = 0;
+        for (int m = 1; m <= m_e; ++m)
+            for (int s = -1; s <= 1; s += 2) {
+                bool ok = true;
+                int dot = 0;
+                for (int q = 0; q < d; ++q) {
+                    int v = (jc[q] - s * m * ee[q]) % N;
+                    if (v < 0) v += N;
+                    if (v > N / 2) v -= N;  // centred representative (|l| <= Ñ < N/2)
+                    if (v > Nt || v < -Nt) ok = false;
+                    dot += v * ee[q];
+                }
+                if (ok && dot == 0) ++cnt;
+            }
+        if (cnt) acc += aw[di] * cnt;
+    }
+    lam[j] = acc;
+}
+
+__global__ void k_take_real(const double2 *z, int64_t n, double *out)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = z[i].x;
+}
+
+template <int N>
+dvm_status_t fft_pass(dvm_plan_s *P, const FftArgs &a)
+{
+    constexpr int B = (1024 / N) < N ? (1024 / N) : N;
+    int64_t nodes = 1;
+    for (int j = 0; j < a.d; ++j) nodes *= N;
+    const int64_t tiles = a.npairs * (nodes / N / B);
+    LaunchScope ls(P, KC_FFT);
+    k_fft_pass<N><<<(unsigned)tiles, kFT, 0, P->stream>>>(a);
+    DVM_CUDA(cudaGetLastError());
+    return DVM_OK;
+}
+
+dvm_status_t fft_dispatch(dvm_plan_s *P, const FftArgs &a)
+{
+    switch (P->N) {
+    case 16: return fft_pass<16>(P, a);
+    case 32: return fft_pass<32>(P, a);
+    case 64: return fft_pass<64>(P, a);
+    case 128: return fft_pass<128>(P, a);
+    case 256: return fft_pass<256>(P, a);
+    default: set_error("FFT length unsupported"); return DVM_E_UNSUPPORTED;
+    }
+}
+
+}  // namespace
+
+
+// Plan-time tables of the loss: twiddles, λ of the plan's (local) directions
+// and its real spectrum λ̂.
+dvm_status_t build_loss(dvm_plan_s *P)
+{
+    const int d = P->d, N = P->N;
+    int64_t nodes = 1;
+    for (int j = 0; j < d; ++j) nodes *= N;
+    GainTables &g = P->g;
+    DVM_CUDA(cudaMalloc(&g.tw, sizeof(double2) * N / 2));
+    DVM_CUDA(cudaMalloc(&g.lamhat, sizeof(double) * nodes));
+    g.bytes += sizeof(double2) * N / 2 + sizeof(double) * nodes;
+    {
+        LaunchScope ls(P, KC_PLAN);
+        k_twiddles<<<1, 128, 0, P->stream>>>(N, g.tw);
+    }
+    double *lam = nullptr;
+    double2 *z = nullptr;
+    DVM_CUDA(cudaMalloc(&lam, sizeof(double) * nodes));
+    DVM_CUDA(cudaMalloc(&z, sizeof(double2) * nodes));
+    {
+        LaunchScope ls(P, KC_PLAN);
+        k_lambda<<<(unsigned)((nodes + 127) / 128), 128, 0, P->stream>>>(d, N, P->p, P->Ntilde, P->t.local,
+                                                                         (int)P->local.size(), P->t.e, P->t.M,
+                                                                         P->t.a, lam);
+    }
+    const cudaError_t le = cudaGetLastError();
+    dvm_status_t st = le == cudaSuccess ? DVM_OK : cuda_fail(le, "k_lambda");
+    for (int k = 0; k < d && !st; ++k) {
+        FftArgs a = {};
+        a.d = d;
+        a.npairs = 1;
+        a.tw = g.tw;
+        a.r_cells = 1;
+        a.r_first = 0;
+        a.ax = d - 1 - k;
+        a.zin = z;
+        a.zout = z;
+        if (k == 0) {
+            a.r0 = lam;
+            a.r_stride = nodes;
+        }
+        st = fft_dispatch(P, a);
+    }
+    if (!st) {
+        LaunchScope ls(P, KC_PLAN);
+        k_take_real<<<256, 256, 0, P->stream>>>(z, nodes, g.lamhat);
+    }
+    cudaStreamSynchronize(P->stream);
+    cudaFree(lam);
+    cudaFree(z);
+    if (st) return st;
+    DVM_CUDA(cudaGetLastError());
+    return DVM_OK;
+}
+
+// Loss initialisation Q[c] := −f[c] Λ[c] for cells [0, ncells) (Λ = λ ⊛ f).
+dvm_status_t loss_init(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q, int64_t q_stride, int64_t ncells,
+                       double2 *QI)
+{
+    const int d = P->d;
+    int64_t nodes = 1;
+    for (int j = 0; j < d; ++j) nodes *= P->N;
+    const int64_t npairs_all = (ncells + 1) / 2;
+    const int64_t batch = std::max<int64_t>(1, std::min<int64_t>(npairs_all, (int64_t)((256ull << 20) / (16 * nodes))));
+    Workspace &w = P->ws;
+    dvm_status_t st;
+    if ((st = grow(&w.fft_z, &w.fft_z_elems, (size_t)(batch * nodes), P->stream))) return st;
+    double scale = 1.0 / (double)nodes;
+    for (int64_t p0 = 0; p0 < npairs_all; p0 += batch) {
+        const int64_t np = std::min(batch, npairs_all - p0);
+        for (int k = 0; k < 2 * d; ++k) {
+            FftArgs a = {};
+            a.d = d;
+            a.npairs = np;
+            a.tw = P->g.tw;
+            a.r_cells = ncells;
+            a.r_first = 2 * p0;
+            const bool fwd = k < d;
+            a.inverse = fwd ? 0 : 1;
+            a.ax = fwd ? d - 1 - k : k - d;
+            a.zin = w.fft_z;
+            a.zout = w.fft_z;
+            if (k == 0) {
+                a.r0 = f;
+                a.r_stride = f_stride;
+            }
+            if (k == d - 1) a.mult = P->g.lamhat;
+            if (k == 2 * d - 1) {
+                a.qI = QI;
+                a.q = Q;
+                a.q_stride = q_stride;
+                a.f = f;
+                a.f_stride = f_stride;
+                a.scale = scale;
+            }
+            if ((st = fft_dispatch(P, a))) return st;
+        }
+    }
+    return DVM_OK;
+}
+
+
+}  // namespace dvm

@@ -1,0 +1,252 @@
+// dvm_pair2d.cu -- 2D evaluation of Q = D^{Ñ,N̄}(f,f) (Maxwell molecules).
+//
+// In 2D the perp set of direction e is the line P_e = {n e⊥ : |n| <= M_e}
+// and e⊥ is again a direction of the table with the same
+// M_e and a_e (|e⊥| = |e|, |e⊥|_inf = |e|_inf).  With the inclusive line windows
+//     W_e(x) = Σ_{|m| <= M_e} f(x + m e)
+// the factors of eq:decD are S_e = W_e − f and T_e = W_{e⊥}, so a pair of
+// directions {e, e⊥} contributes
+//     G_e + G_{e⊥} = a_e [ (W_e − f) W_{e⊥} + (W_{e⊥} − f) W_e ]
+// (each term only if that direction belongs to the plan's shard).  The loss is
+// the FFT convolution −f (λ ⊛ f) of dvm_loss.cu (reading R21).
+//
+//   k_wline2d  W along the first direction of every pair unit (sliding window
+//              along its lattice lines) -> scratch
+//   k_pair2d   W along the second direction (always one with an odd first
+//              component: its lines start on the transversal x0 = 0 and warp
+//              lanes walk adjacent lines, so every access is coalesced), combined
+//              with the scratch and f into one partial gain per pair unit
+//   k_sum_units Q += Σ_units partial in unit order (bitwise deterministic)
+#include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "dvm_internal.h"
+
+namespace dvm {
+namespace {
+
+constexpr int kPT = 128;  // threads per CTA
+
+struct Unit2D {
+    int a0, a1;   // first direction A (pass 1)
+    int b0, b1;   // second direction B (pass 2, odd first component)
+    int M;        // common M_e
+    int flags;    // bit0: A is local, bit1: B is local
+    double aw;    // common a_e
+};
+
+__device__ __forceinline__ uint32_t pk2(int c0, int c1, int p, int N)
+{
+    return ((uint32_t)(c0 & (N - 1)) << p) | (uint32_t)(c1 & (N - 1));
+}
+
+// Lines of a primitive v in Z_N^2 (N = 2^p) have length N; if v0 is odd each
+// line meets x0 = 0 exactly once (start (0, j)), else v1 is odd and x1 = 0 is
+// the transversal (start (j, 0)).  Work item = (line j, segment s).
+struct LineWalk {
+    uint32_t x;     // packed current node
+    uint32_t step;  // packed v
+    uint32_t fwd;   // packed (M+1) v
+    uint32_t back;  // packed -M v
+};
+
+__device__ __forceinline__ LineWalk line_start(int v0, int v1, int M, int j, int s, int seglen, int p, int N)
+{
+    LineWalk w;
+    const int t0 = s * seglen;
+    if (v0 & 1)
+        w.x = pk2(t0 * v0, j + t0 * v1, p, N);
+    else
+        w.x = pk2(j + t0 * v0, t0 * v1, p, N);
+    w.step = pk2(v0, v1, p, N);
+    w.fwd = pk2((M + 1) * v0, (M + 1) * v1, p, N);
+    w.back = pk2(-M * v0, -M * v1, p, N);
+    return w;
+}
+
+__device__ __forceinline__ double window_at(const double *__restrict__ fc, uint32_t x, int v0, int v1, int M, int p,
+                                            int N, uint32_t H)
+{
+    double W = 0.0;
+    for (int m = -M; m <= M; ++m) W += __ldg(fc + swar_add(x, pk2(m * v0, m * v1, p, N), H));
+    return W;
+}
+
+// pass 1: scratch[u][c][x] = W_A(x)
+__global__ void __launch_bounds__(kPT) k_wline2d(const double *__restrict__ f, int64_t f_stride, int ncells,
+                                                 const Unit2D *__restrict__ units, int p, int N, uint32_t H,
+                                                 int seglen, double *__restrict__ scratch)
+{
+    const int u = blockIdx.y, c = blockIdx.z;
+    const Unit2D U = units[u];
+    const int64_t nodes = (int64_t)N * N;
+    const double *fc = f + (int64_t)c * f_stride;
+    double *out = scratch + ((int64_t)u * ncells + c) * nodes;
+    const int nseg = N / seglen;
+    const int item = blockIdx.x * kPT + threadIdx.x;
+    if (item >= N * nseg) return;
+    const int j = item % N, s = item / N;  // lanes on adjacent lines
+    LineWalk w = line_start(U.a0, U.a1, U.M, j, s, seglen, p, N);
+    double W = window_at(fc, w.x, U.a0, U.a1, U.M, p, N, H);
+#pragma unroll 4
+    for (int i = 0; i < seglen; ++i) {
+        out[w.x] = W;
+        W += __ldg(fc + swar_add(w.x, w.fwd, H)) - __ldg(fc + swar_add(w.x, w.back, H));
+        w.x = swar_add(w.x, w.step, H);
+    }
+}
+
+// pass 2: part[u][c][x] = a [A local](W_A − f) W_B + a [B local](W_B − f) W_A
+__global__ void __launch_bounds__(kPT) k_pair2d(const double *__restrict__ f, int64_t f_stride, int ncells,
+                                                const Unit2D *__restrict__ units, int p, int N, uint32_t H,
+                                                int seglen, const double *__restrict__ scratch,
+                                                double *__restrict__ part)
+{
+    const int u = blockIdx.y, c = blockIdx.z;
+    const Unit2D U = units[u];
+    const int64_t nodes = (int64_t)N * N;
+    const double *fc = f + (int64_t)c * f_stride;
+    const double *WA = scratch + ((int64_t)u * ncells + c) * nodes;
+    double *out = part + ((int64_t)u * ncells + c) * nodes;
+    const int nseg = N / seglen;
+    const int item = blockIdx.x * kPT + threadIdx.x;
+    if (item >= N * nseg) return;
+    const int j = item % N, s = item / N;
+    LineWalk w = line_start(U.b0, U.b1, U.M, j, s, seglen, p, N);
+    double W = window_at(fc, w.x, U.b0, U.b1, U.M, p, N, H);
+    const double ca = (U.flags & 1) ? U.aw : 0.0, cb = (U.flags & 2) ? U.aw : 0.0;
+#pragma unroll 4
+    for (int i = 0; i < seglen; ++i) {
+        const double wa = WA[w.x], f0 = __ldg(fc + w.x);
+        out[w.x] = ca * (wa - f0) * W + cb * (W - f0) * wa;
+        W += __ldg(fc + swar_add(w.x, w.fwd, H)) - __ldg(fc + swar_add(w.x, w.back, H));
+        w.x = swar_add(w.x, w.step, H);
+    }
+}
+
+// Q[c][x] += Σ_u part[u][c][x], u ascending
+__global__ void k_sum_units(const double *__restrict__ part, int nunits, int ncells, int64_t nodes,
+                            double *__restrict__ Q, int64_t q_stride)
+{
+    const int64_t total = (int64_t)ncells * nodes;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = i / nodes, x = i % nodes;
+        double acc = Q[c * q_stride + x];
+        for (int u = 0; u < nunits; ++u) acc += part[(int64_t)u * total + i];
+        Q[c * q_stride + x] = acc;
+    }
+}
+
+}  // namespace
+
+// Plan-time: pair units of the (local) directions, loss tables.
+dvm_status_t build_pair2d(dvm_plan_s *P)
+{
+    if (P->d != 2 || P->N < 16 || P->N > 256) return DVM_OK;  // FFT lengths of dvm_loss.cu; else v1
+    const int A = P->A;
+    auto canon = [](int a, int b) {
+        if (a < 0 || (a == 0 && b < 0)) {
+            a = -a;
+            b = -b;
+        }
+        return std::make_pair(a, b);
+    };
+    auto find = [&](int a, int b) {
+        for (int i = 0; i < A; ++i)
+            if (P->h_e[3 * i] == a && P->h_e[3 * i + 1] == b) return i;
+        return -1;
+    };
+    std::vector<Unit2D> units;
+    std::vector<uint8_t> used(A, 0);
+    for (int i = 0; i < A; ++i) {
+        if (used[i]) continue;
+        const int e0 = P->h_e[3 * i], e1 = P->h_e[3 * i + 1];
+        const auto pp = canon(-e1, e0);
+        const int k = find(pp.first, pp.second);
+        if (k < 0 || P->h_M[k] != P->h_M[i]) {
+            set_error("2D direction table is not closed under e -> e^perp");
+            return DVM_E_UNSUPPORTED;
+        }
+        used[i] = used[k] = 1;
+        const bool li = P->is_local[i], lk = P->is_local[k];
+        if (!li && !lk) continue;
+        Unit2D U;
+        // pass 2 (coalesced) takes the direction with an odd first component
+        const bool i_second = (e0 & 1) != 0;
+        const int sA = i_second ? k : i, sB = i_second ? i : k;
+        U.a0 = P->h_e[3 * sA];
+        U.a1 = P->h_e[3 * sA + 1];
+        U.b0 = P->h_e[3 * sB];
+        U.b1 = P->h_e[3 * sB + 1];
+        U.M = P->h_M[i];
+        U.flags = (P->is_local[sA] ? 1 : 0) | (P->is_local[sB] ? 2 : 0);
+        U.aw = P->h_a[i];
+        units.push_back(U);
+    }
+    P->g.nunits = (int)units.size();
+    if (!units.empty()) {
+        DVM_CUDA(cudaMalloc(&P->g.units, sizeof(Unit2D) * units.size()));
+        DVM_CUDA(cudaMemcpyAsync(P->g.units, units.data(), sizeof(Unit2D) * units.size(), cudaMemcpyHostToDevice,
+                                 P->stream));
+        P->g.bytes += sizeof(Unit2D) * units.size();
+    }
+    dvm_status_t st = build_loss(P);
+    if (st) return st;
+    DVM_CUDA(cudaStreamSynchronize(P->stream));
+    P->g.ready = true;
+    return DVM_OK;
+}
+
+size_t pair2d_unit_bytes() { return sizeof(Unit2D); }
+
+dvm_status_t collide_pair2d(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q, int64_t q_stride,
+                            int64_t ncells, bool *handled)
+{
+    *handled = false;
+    if (P->d != 2 || !P->g.ready || ncells <= 0) return DVM_OK;
+    *handled = true;
+    const int N = P->N, p = P->p;
+    const int64_t nodes = (int64_t)N * N;
+    // loss: Q := −f Λ for all cells
+    dvm_status_t st = loss_init(P, f, f_stride, Q, q_stride, ncells, nullptr);
+    if (st) return st;
+    const int nunits = P->g.nunits;
+    if (nunits == 0) return DVM_OK;
+    // cell chunks bounded by the scratch + partial budget
+    const size_t per_cell = sizeof(double) * 2 * (size_t)nunits * nodes;
+    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(ncells, (int64_t)((512ull << 20) / per_cell)));
+    Workspace &w = P->ws;
+    if ((st = grow(&w.p2_scr, &w.p2_scr_elems, (size_t)(chunk * nunits * nodes), P->stream))) return st;
+    if ((st = grow(&w.p2_part, &w.p2_part_elems, (size_t)(chunk * nunits * nodes), P->stream))) return st;
+    const int seglen = std::max(16, (int)((nodes + 1023) / 1024));
+    const int items = N * (N / std::min(seglen, N));
+    const int sl = std::min(seglen, N);
+    for (int64_t c0 = 0; c0 < ncells; c0 += chunk) {
+        const int nc = (int)std::min<int64_t>(chunk, ncells - c0);
+        dim3 grid((items + kPT - 1) / kPT, nunits, nc);
+        {
+            LaunchScope ls(P, KC_LINESUM);
+            k_wline2d<<<grid, kPT, 0, P->stream>>>(f + c0 * f_stride, f_stride, nc,
+                                                   reinterpret_cast<const Unit2D *>(P->g.units), p, N, P->pk.H, sl,
+                                                   w.p2_scr);
+        }
+        {
+            LaunchScope ls(P, KC_ROWSUM);
+            k_pair2d<<<grid, kPT, 0, P->stream>>>(f + c0 * f_stride, f_stride, nc,
+                                                  reinterpret_cast<const Unit2D *>(P->g.units), p, N, P->pk.H, sl,
+                                                  w.p2_scr, w.p2_part);
+        }
+        {
+            LaunchScope ls(P, KC_REDUCE);
+            k_sum_units<<<592, 256, 0, P->stream>>>(w.p2_part, nunits, nc, nodes, Q + c0 * q_stride, q_stride);
+        }
+        DVM_CUDA(cudaGetLastError());
+    }
+    return DVM_OK;
+}
+
+}  // namespace dvm

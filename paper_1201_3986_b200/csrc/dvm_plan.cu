@@ -458,6 +458,7 @@ dvm_status_t build_table(dvm_plan_s *P)
                                  P->stream));
     DVM_CUDA(cudaStreamSynchronize(P->stream));
     if ((st = build_gain3d(P))) return st;
+    if ((st = build_pair2d(P))) return st;
     P->table_bytes = acc + P->g.bytes;
     return DVM_OK;
 }

@@ -39,6 +39,9 @@ for name in ("c1", "c2", "c3", "c4", "c5"):
     prof = {k: round(v[0], 4) for k, v in p.profile_read().items() if v[1]}
     p.profile(False)
     ncell = f.shape[0]
+    nodes = cfg.N ** cfg.d
+    eff = (p.A + 2) * 8.0 * nodes * ncell / (ms / 1e3) / 1e9  # streaming formulation, SURVEY 8(d)
     out[name] = {"ms_per_eval_batch": ms, "cells": ncell, "evals_per_s": ncell / (ms / 1e3), "A": p.A,
-                 "Ntilde": p.Ntilde, "kernels_ms": prof}
+                 "Ntilde": p.Ntilde, "effective_streaming_GBps": eff, "kernels_ms": prof}
     print(name, json.dumps(out[name]), flush=True)
+
