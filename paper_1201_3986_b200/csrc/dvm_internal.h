@@ -101,6 +101,7 @@ struct GainTables {
     double *lamhat = nullptr; // [N^d] spectrum of the loss kernel λ (real)
     void *units = nullptr;    // 2D: direction-pair units (dvm_pair2d.cu)
     int nunits = 0;
+    int maxitems2d = 0;       // 2D: work items of the longest line walk
     size_t bytes = 0;
 };
 }  // namespace dvm

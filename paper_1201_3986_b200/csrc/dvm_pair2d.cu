@@ -44,9 +44,13 @@ __device__ __forceinline__ uint32_t pk2(int c0, int c1, int p, int N)
     return ((uint32_t)(c0 & (N - 1)) << p) | (uint32_t)(c1 & (N - 1));
 }
 
-// Lines of a primitive v in Z_N^2 (N = 2^p) have length N; if v0 is odd each
-// line meets x0 = 0 exactly once (start (0, j)), else v1 is odd and x1 = 0 is
-// the transversal (start (j, 0)).  Work item = (line j, segment s).
+// Walks along the lines of a primitive v in Z_N^2 (N = 2^p), coalesced.  With
+// v0 = 2^s · odd (s < p), a line returns to the same row residue every
+// Lv = N / 2^s steps; the segments starting at every node (c, j) of the rows
+// c < 2^s partition all lines, and warp lanes on consecutive columns j stay in
+// one row at every step (consecutive addresses).  Segments are cut further into
+// `seglen` pieces.  v0 = 0 (v = (0, ±1): the lines are the rows) walks from the
+// column x1 = 0 instead (strided, one direction only).
 struct LineWalk {
     uint32_t x;     // packed current node
     uint32_t step;  // packed v
@@ -54,14 +58,47 @@ struct LineWalk {
     uint32_t back;  // packed -M v
 };
 
-__device__ __forceinline__ LineWalk line_start(int v0, int v1, int M, int j, int s, int seglen, int p, int N)
+struct WalkShape {
+    int R;       // rows of starts (2^s), N for v0 == 0 (see below)
+    int seglen;  // steps per work item
+    int nsub;    // work items per (row, column) start
+};
+
+__host__ __device__ inline WalkShape walk_shape(int v0, int N)
+{
+    WalkShape w;
+    int R = 1;
+    if (v0 == 0) {
+        R = 0;  // rows as lines: starts (j, 0), one item per line
+        w.R = 0;
+        w.seglen = N;
+        w.nsub = 1;
+        return w;
+    }
+    int a = v0 < 0 ? -v0 : v0;
+    while (!(a & 1) && R < N) {
+        a >>= 1;
+        R <<= 1;
+    }
+    const int Lv = N / R;
+    w.R = R;
+    w.seglen = Lv < 64 ? Lv : 64;
+    w.nsub = Lv / w.seglen;
+    return w;
+}
+
+__host__ __device__ inline int walk_items(const WalkShape &w, int N) { return w.R == 0 ? N : w.nsub * w.R * N; }
+
+__device__ __forceinline__ LineWalk line_start(int v0, int v1, int M, int item, const WalkShape &ws, int p, int N)
 {
     LineWalk w;
-    const int t0 = s * seglen;
-    if (v0 & 1)
-        w.x = pk2(t0 * v0, j + t0 * v1, p, N);
-    else
-        w.x = pk2(j + t0 * v0, t0 * v1, p, N);
+    if (ws.R == 0) {
+        w.x = pk2(item, 0, p, N);
+    } else {
+        const int j = item % N, c = (item / N) % ws.R, k = item / (N * ws.R);
+        const int t0 = k * ws.seglen;
+        w.x = pk2(c + t0 * v0, j + t0 * v1, p, N);
+    }
     w.step = pk2(v0, v1, p, N);
     w.fwd = pk2((M + 1) * v0, (M + 1) * v1, p, N);
     w.back = pk2(-M * v0, -M * v1, p, N);
@@ -79,21 +116,20 @@ __device__ __forceinline__ double window_at(const double *__restrict__ fc, uint3
 // pass 1: scratch[u][c][x] = W_A(x)
 __global__ void __launch_bounds__(kPT) k_wline2d(const double *__restrict__ f, int64_t f_stride, int ncells,
                                                  const Unit2D *__restrict__ units, int p, int N, uint32_t H,
-                                                 int seglen, double *__restrict__ scratch)
+                                                 double *__restrict__ scratch)
 {
     const int u = blockIdx.y, c = blockIdx.z;
     const Unit2D U = units[u];
     const int64_t nodes = (int64_t)N * N;
     const double *fc = f + (int64_t)c * f_stride;
     double *out = scratch + ((int64_t)u * ncells + c) * nodes;
-    const int nseg = N / seglen;
+    const WalkShape ws = walk_shape(U.a0, N);
     const int item = blockIdx.x * kPT + threadIdx.x;
-    if (item >= N * nseg) return;
-    const int j = item % N, s = item / N;  // lanes on adjacent lines
-    LineWalk w = line_start(U.a0, U.a1, U.M, j, s, seglen, p, N);
+    if (item >= walk_items(ws, N)) return;
+    LineWalk w = line_start(U.a0, U.a1, U.M, item, ws, p, N);
     double W = window_at(fc, w.x, U.a0, U.a1, U.M, p, N, H);
 #pragma unroll 4
-    for (int i = 0; i < seglen; ++i) {
+    for (int i = 0; i < ws.seglen; ++i) {
         out[w.x] = W;
         W += __ldg(fc + swar_add(w.x, w.fwd, H)) - __ldg(fc + swar_add(w.x, w.back, H));
         w.x = swar_add(w.x, w.step, H);
@@ -103,7 +139,7 @@ __global__ void __launch_bounds__(kPT) k_wline2d(const double *__restrict__ f, i
 // pass 2: part[u][c][x] = a [A local](W_A − f) W_B + a [B local](W_B − f) W_A
 __global__ void __launch_bounds__(kPT) k_pair2d(const double *__restrict__ f, int64_t f_stride, int ncells,
                                                 const Unit2D *__restrict__ units, int p, int N, uint32_t H,
-                                                int seglen, const double *__restrict__ scratch,
+                                                const double *__restrict__ scratch,
                                                 double *__restrict__ part)
 {
     const int u = blockIdx.y, c = blockIdx.z;
@@ -112,15 +148,14 @@ __global__ void __launch_bounds__(kPT) k_pair2d(const double *__restrict__ f, in
     const double *fc = f + (int64_t)c * f_stride;
     const double *WA = scratch + ((int64_t)u * ncells + c) * nodes;
     double *out = part + ((int64_t)u * ncells + c) * nodes;
-    const int nseg = N / seglen;
+    const WalkShape ws = walk_shape(U.b0, N);
     const int item = blockIdx.x * kPT + threadIdx.x;
-    if (item >= N * nseg) return;
-    const int j = item % N, s = item / N;
-    LineWalk w = line_start(U.b0, U.b1, U.M, j, s, seglen, p, N);
+    if (item >= walk_items(ws, N)) return;
+    LineWalk w = line_start(U.b0, U.b1, U.M, item, ws, p, N);
     double W = window_at(fc, w.x, U.b0, U.b1, U.M, p, N, H);
     const double ca = (U.flags & 1) ? U.aw : 0.0, cb = (U.flags & 2) ? U.aw : 0.0;
 #pragma unroll 4
-    for (int i = 0; i < seglen; ++i) {
+    for (int i = 0; i < ws.seglen; ++i) {
         const double wa = WA[w.x], f0 = __ldg(fc + w.x);
         out[w.x] = ca * (wa - f0) * W + cb * (W - f0) * wa;
         W += __ldg(fc + swar_add(w.x, w.fwd, H)) - __ldg(fc + swar_add(w.x, w.back, H));
@@ -188,6 +223,10 @@ dvm_status_t build_pair2d(dvm_plan_s *P)
         units.push_back(U);
     }
     P->g.nunits = (int)units.size();
+    int maxitems = 1;
+    for (const Unit2D &U : units)
+        maxitems = std::max({maxitems, walk_items(walk_shape(U.a0, P->N), P->N), walk_items(walk_shape(U.b0, P->N), P->N)});
+    P->g.maxitems2d = maxitems;
     if (!units.empty()) {
         DVM_CUDA(cudaMalloc(&P->g.units, sizeof(Unit2D) * units.size()));
         DVM_CUDA(cudaMemcpyAsync(P->g.units, units.data(), sizeof(Unit2D) * units.size(), cudaMemcpyHostToDevice,
@@ -222,22 +261,20 @@ dvm_status_t collide_pair2d(dvm_plan_s *P, const double *f, int64_t f_stride, do
     Workspace &w = P->ws;
     if ((st = grow(&w.p2_scr, &w.p2_scr_elems, (size_t)(chunk * nunits * nodes), P->stream))) return st;
     if ((st = grow(&w.p2_part, &w.p2_part_elems, (size_t)(chunk * nunits * nodes), P->stream))) return st;
-    const int seglen = std::max(16, (int)((nodes + 1023) / 1024));
-    const int items = N * (N / std::min(seglen, N));
-    const int sl = std::min(seglen, N);
+    const int items = P->g.maxitems2d;  // largest walk of any unit (shorter walks exit early)
     for (int64_t c0 = 0; c0 < ncells; c0 += chunk) {
         const int nc = (int)std::min<int64_t>(chunk, ncells - c0);
         dim3 grid((items + kPT - 1) / kPT, nunits, nc);
         {
             LaunchScope ls(P, KC_LINESUM);
             k_wline2d<<<grid, kPT, 0, P->stream>>>(f + c0 * f_stride, f_stride, nc,
-                                                   reinterpret_cast<const Unit2D *>(P->g.units), p, N, P->pk.H, sl,
+                                                   reinterpret_cast<const Unit2D *>(P->g.units), p, N, P->pk.H,
                                                    w.p2_scr);
         }
         {
             LaunchScope ls(P, KC_ROWSUM);
             k_pair2d<<<grid, kPT, 0, P->stream>>>(f + c0 * f_stride, f_stride, nc,
-                                                  reinterpret_cast<const Unit2D *>(P->g.units), p, N, P->pk.H, sl,
+                                                  reinterpret_cast<const Unit2D *>(P->g.units), p, N, P->pk.H,
                                                   w.p2_scr, w.p2_part);
         }
         {
