@@ -35,8 +35,8 @@
  *     message for the last failure on the calling thread.
  *   - Threading: one host thread per plan at a time; distinct plans are
  *     independent.
- *   - Determinism: for a fixed plan, input and device the result is bitwise
- *     reproducible (no floating-point atomics on the accumulation path).
+ *   - Determinism: for a fixed plan, input (batch) and device the result is
+ *     bitwise reproducible (no floating-point atomics on the accumulation path).
  */
 #ifndef DVM_H
 #define DVM_H
@@ -132,7 +132,9 @@ DVM_API dvm_status_t dvm_set_stream(dvm_plan_t plan, void *stream);
 DVM_API dvm_status_t dvm_collide(dvm_plan_t plan, const double *f, double *Q);
 
 /* Same for ncells cells; cell c occupies [c*cell_stride, c*cell_stride + N^d)
- * of f and of Q (cell_stride 0 -> N^d). */
+ * of f and of Q (cell_stride 0 -> N^d).  The plan grows a device workspace on
+ * first use of a batch size (3D: ~2 × 16 B per node per cell pair plus a 256 MiB
+ * FFT batch; 2D: ≤ 512 MiB of per-pair partials); DVM_E_NOMEM if it cannot. */
 DVM_API dvm_status_t dvm_collide_batched(dvm_plan_t plan, const double *f, double *Q, int64_t ncells,
                                  int64_t cell_stride);
 
@@ -162,9 +164,14 @@ DVM_API dvm_status_t dvm_profile_enable(dvm_plan_t plan, int enable);
 DVM_API dvm_status_t dvm_profile_read(dvm_plan_t plan, double *ms, uint64_t *count, int n);
 DVM_API const char *dvm_profile_name(int k);
 
-/* Evaluation path: 0 = default (3D N in {32,64,128}: cluster-per-cell plane
- * kernel; otherwise orbit sweeps), 1 = orbit sweeps only (v1, cross-checks).
- * Both compute the same operator; results agree to rounding. */
+/* Evaluation path: 0 = default, 1 = orbit sweeps only (v1, cross-checks).
+ * Default: 3D with N in {32, 64}: the loss as one FFT convolution f (λ ⊛ f)
+ * (reading R21) and the gain by the frame-plane kernel (two cells per node,
+ * warp-specialised, TMEM accumulators); 2D with 16 <= N <= 256: the same FFT
+ * loss and the gain by direction pairs {e, e⊥}; other sizes: v1.  All paths
+ * compute the same operator; results agree to rounding (the FFT loss pairs
+ * cells in one complex transform, so a cell's last bits may depend on its
+ * batch partner; a repeated identical call is bitwise reproducible). */
 DVM_API dvm_status_t dvm_set_path(dvm_plan_t plan, int path);
 
 /* Wait for all work issued on the plan's stream; reports asynchronous faults. */

@@ -14,11 +14,11 @@
 // entries, evaluated as differences of in-row prefix sums).  The basis is
 // chosen per direction to minimise the smem loads of that program.
 //
-// Runs.  ê_2 (the fastest storage axis) = e_2 z + a2 u + b2 w: the storage
-// neighbours x, x + ê_2 lie in planes γ, γ + e_2 at in-plane offset (a2, b2).
-// The kernel gathers/scatters planes in pairs {γ, γ + e_2} so that every
-// memory access is a 16-byte run; for e_2 = 0 the frame uses u = ê_2 and each
-// plane row is one contiguous storage row.
+// Storage runs.  For e_2 = 0 the frame uses u = ê_2 (the fastest storage
+// axis), so every plane row is one contiguous storage row and the kernel's
+// gathers and stores are coalesced.  (a2, b2) with ê_2 = e_2 z + a2 u + b2 w
+// locate the storage neighbour x + ê_2 in the frame (checked by
+// tools/frame_check.cpp).
 #pragma once
 
 #include <stdint.h>
