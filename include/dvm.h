@@ -153,6 +153,16 @@ DVM_API dvm_status_t dvm_moments(dvm_plan_t plan, const double *f, double *out_h
  * d+2 moments (before the first step and after every step).  Synchronous. */
 DVM_API dvm_status_t dvm_euler(dvm_plan_t plan, double *f, double dt, int nsteps, double *moments_host);
 
+/* Second-order TVD Runge-Kutta (Heun) f1 = f + dt D(f,f), f <- (f + f1 +
+ * dt D(f1,f1)) / 2, the time discretisation of PAPER.md:946-947; otherwise as
+ * dvm_euler.  Both steppers run step 1 directly and replay steps 2..nsteps as
+ * one captured CUDA graph on a plan-owned stream (ordered after and before the
+ * plan's stream); results are identical to direct launches. */
+DVM_API dvm_status_t dvm_rk2(dvm_plan_t plan, double *f, double dt, int nsteps, double *moments_host);
+
+/* Enable (default) or disable the CUDA-graph replay of the time steppers. */
+DVM_API dvm_status_t dvm_set_graphs(dvm_plan_t plan, int enable);
+
 /* Per-kernel timing with CUDA events recorded on the plan's stream around
  * every launch (for bench.py's roofline; adds one event pair per launch).
  * enable != 0 clears previous records and starts recording; 0 stops. */
@@ -164,14 +174,16 @@ DVM_API dvm_status_t dvm_profile_enable(dvm_plan_t plan, int enable);
 DVM_API dvm_status_t dvm_profile_read(dvm_plan_t plan, double *ms, uint64_t *count, int n);
 DVM_API const char *dvm_profile_name(int k);
 
-/* Evaluation path: 0 = default, 1 = orbit sweeps only (v1, cross-checks).
- * Default: 3D with N in {32, 64}: the loss as one FFT convolution f (λ ⊛ f)
- * (reading R21) and the gain by the frame-plane kernel (two cells per node,
- * warp-specialised, TMEM accumulators); 2D with 16 <= N <= 256: the same FFT
- * loss and the gain by direction pairs {e, e⊥}; other sizes: v1.  All paths
- * compute the same operator; results agree to rounding (the FFT loss pairs
- * cells in one complex transform, so a cell's last bits may depend on its
- * batch partner; a repeated identical call is bitwise reproducible). */
+/* Evaluation path: 0 = auto (default), 1 = v1 orbit sweeps only, 2 = the
+ * FFT-loss paths whenever the plan built them.  The FFT-loss paths evaluate
+ * the loss as one FFT convolution f (λ ⊛ f) (reading R21): 3D with N in
+ * {32, 64}: gain by the frame-plane kernel (two cells per node,
+ * warp-specialised, TMEM accumulators); 2D with 16 <= N <= 256: gain by
+ * direction pairs {e, e⊥}.  Auto picks them for 3D and for 2D N >= 128 (below
+ * that the v1 sweeps are faster), v1 otherwise.  All paths compute the same
+ * operator; results agree to rounding (the FFT loss pairs cells in one complex
+ * transform, so a cell's last bits may depend on its batch partner; a repeated
+ * identical call is bitwise reproducible). */
 DVM_API dvm_status_t dvm_set_path(dvm_plan_t plan, int path);
 
 /* Wait for all work issued on the plan's stream; reports asynchronous faults. */

@@ -351,7 +351,31 @@ dvm_status_t dvm_moments(dvm_plan_t P, const double *f, double *out_host)
     return DVM_OK;
 }
 
-dvm_status_t dvm_euler(dvm_plan_t P, double *f, double dt, int nsteps, double *moments_host)
+// One explicit step of `scheme` (1: Euler f += dt Q(f); 2: TVD-RK2 / Heun,
+// f1 = f + dt Q(f), f = (f + f1 + dt Q(f1)) / 2), then the
+// moments row (device counter) if requested.
+static dvm_status_t one_step(dvm_plan_s *P, int scheme, double *f, double dt, bool mom)
+{
+    const int64_t nodes = nodes_of(P);
+    Workspace &w = P->ws;
+    dvm_status_t st;
+    if ((st = collide_batched(P, f, w.qtmp, 1, nodes))) return st;
+    if (scheme == 1) {
+        if ((st = axpy(P, f, w.qtmp, dt))) return st;
+    } else {
+        if ((st = rk2_stage(P, 1, f, w.f1tmp, w.qtmp, dt))) return st;
+        if ((st = collide_batched(P, w.f1tmp, w.qtmp, 1, nodes))) return st;
+        if ((st = rk2_stage(P, 2, f, w.f1tmp, w.qtmp, dt))) return st;
+    }
+    if (mom && (st = moments_ctr(P, f, w.mom_dev, w.mom_ctr))) return st;
+    return DVM_OK;
+}
+
+// nsteps steps of `scheme`; step 1 runs directly (it sizes every workspace),
+// steps 2..nsteps replay one captured CUDA graph of a step on a plan-owned
+// stream joined to the plan's stream by events (the launch-bound loop of the
+// small grids).  Moments rows: 0 = initial state, s = after step s.
+static dvm_status_t time_stepper(dvm_plan_s *P, int scheme, double *f, double dt, int nsteps, double *moments_host)
 {
     if (!P || !f) {
         set_error("NULL argument");
@@ -364,6 +388,7 @@ dvm_status_t dvm_euler(dvm_plan_t P, double *f, double dt, int nsteps, double *m
     const int64_t nodes = nodes_of(P);
     Workspace &w = P->ws;
     const size_t rows = (size_t)nsteps + 1;
+    const bool mom = moments_host != nullptr;
     if (!w.mom_dev || w.mom_rows < rows) {
         DVM_CUDA(cudaStreamSynchronize(P->stream));
         if (w.mom_dev) cudaFree(w.mom_dev);
@@ -372,14 +397,58 @@ dvm_status_t dvm_euler(dvm_plan_t P, double *f, double dt, int nsteps, double *m
         w.mom_rows = rows;
     }
     if (!w.qtmp) DVM_CUDA(cudaMalloc(&w.qtmp, sizeof(double) * nodes));
+    if (scheme == 2 && !w.f1tmp) DVM_CUDA(cudaMalloc(&w.f1tmp, sizeof(double) * nodes));
+    if (!w.mom_ctr) DVM_CUDA(cudaMalloc(&w.mom_ctr, sizeof(int)));
+    DVM_CUDA(cudaMemsetAsync(w.mom_ctr, 0, sizeof(int), P->stream));
     dvm_status_t st;
-    for (int s = 0; s < nsteps; ++s) {
-        if (moments_host && (st = moments(P, f, w.mom_dev + (size_t)s * (kMaxD + 2)))) return st;
-        if ((st = collide_batched(P, f, w.qtmp, 1, nodes))) return st;
-        if ((st = axpy(P, f, w.qtmp, dt))) return st;
+    if (mom && (st = moments_ctr(P, f, w.mom_dev, w.mom_ctr))) return st;
+    if (nsteps >= 1 && (st = one_step(P, scheme, f, dt, mom))) return st;
+    int done = nsteps >= 1 ? 1 : 0;
+    if (nsteps >= 2 && P->use_graphs) {
+        if (!P->gstream) {
+            DVM_CUDA(cudaStreamCreateWithFlags(&P->gstream, cudaStreamNonBlocking));
+            DVM_CUDA(cudaEventCreateWithFlags(&P->gev[0], cudaEventDisableTiming));
+            DVM_CUDA(cudaEventCreateWithFlags(&P->gev[1], cudaEventDisableTiming));
+        }
+        DVM_CUDA(cudaEventRecord(P->gev[0], P->stream));
+        DVM_CUDA(cudaStreamWaitEvent(P->gstream, P->gev[0], 0));
+        cudaStream_t user = P->stream;
+        const bool prof = P->profiling;
+        const uint64_t l0 = P->launches;
+        P->stream = P->gstream;
+        P->profiling = false;  // no event records inside the captured step
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        cudaError_t ce = cudaStreamBeginCapture(P->gstream, cudaStreamCaptureModeThreadLocal);
+        if (ce == cudaSuccess) {
+            st = one_step(P, scheme, f, dt, mom);
+            ce = cudaStreamEndCapture(P->gstream, &graph);
+            if (st == DVM_OK && ce == cudaSuccess) ce = cudaGraphInstantiate(&exec, graph, 0);
+        }
+        const uint64_t per_step = P->launches - l0;
+        P->stream = user;
+        P->profiling = prof;
+        if (st == DVM_OK && ce == cudaSuccess && exec) {
+            for (int s = done; s < nsteps; ++s) {
+                ce = cudaGraphLaunch(exec, P->gstream);
+                if (ce != cudaSuccess) break;
+            }
+            P->launches += per_step * (uint64_t)(nsteps - done - 1);  // the capture counted one step
+            if (ce == cudaSuccess) done = nsteps;
+        } else {
+            P->launches = l0;
+            cudaGetLastError();  // capture unsupported here: fall back to direct launches
+            st = DVM_OK;
+        }
+        if (exec) cudaGraphExecDestroy(exec);
+        if (graph) cudaGraphDestroy(graph);
+        DVM_CUDA(cudaEventRecord(P->gev[1], P->gstream));
+        DVM_CUDA(cudaStreamWaitEvent(P->stream, P->gev[1], 0));
+        if (ce != cudaSuccess && done != nsteps) return cuda_fail(ce, "cudaGraphLaunch");
     }
-    if (moments_host) {
-        if ((st = moments(P, f, w.mom_dev + (size_t)nsteps * (kMaxD + 2)))) return st;
+    for (int s = done; s < nsteps; ++s)
+        if ((st = one_step(P, scheme, f, dt, mom))) return st;
+    if (mom) {
         std::string buf;
         buf.resize(sizeof(double) * (kMaxD + 2) * rows);
         DVM_CUDA(cudaMemcpyAsync(&buf[0], w.mom_dev, buf.size(), cudaMemcpyDeviceToHost, P->stream));
@@ -390,6 +459,26 @@ dvm_status_t dvm_euler(dvm_plan_t P, double *f, double dt, int nsteps, double *m
     } else {
         DVM_CUDA(cudaStreamSynchronize(P->stream));
     }
+    return DVM_OK;
+}
+
+dvm_status_t dvm_euler(dvm_plan_t P, double *f, double dt, int nsteps, double *moments_host)
+{
+    return time_stepper(P, 1, f, dt, nsteps, moments_host);
+}
+
+dvm_status_t dvm_rk2(dvm_plan_t P, double *f, double dt, int nsteps, double *moments_host)
+{
+    return time_stepper(P, 2, f, dt, nsteps, moments_host);
+}
+
+dvm_status_t dvm_set_graphs(dvm_plan_t P, int enable)
+{
+    if (!P) {
+        set_error("NULL argument");
+        return DVM_E_NULL;
+    }
+    P->use_graphs = enable != 0;
     return DVM_OK;
 }
 
@@ -437,11 +526,11 @@ dvm_status_t dvm_set_path(dvm_plan_t P, int path)
         set_error("NULL argument");
         return DVM_E_NULL;
     }
-    if (path != 0 && path != 1) {
-        set_error("path must be 0 (default) or 1 (v1 orbit sweeps)");
+    if (path < 0 || path > 2) {
+        set_error("path must be 0 (auto), 1 (v1 orbit sweeps) or 2 (gain3d / pair2d)");
         return DVM_E_STATE;
     }
-    P->force_v1 = path == 1;
+    P->path_mode = path;
     return DVM_OK;
 }
 
@@ -463,6 +552,12 @@ dvm_status_t dvm_plan_destroy(dvm_plan_t P)
         return DVM_E_NULL;
     }
     cudaStreamSynchronize(P->stream);
+    if (P->gstream) {
+        cudaStreamSynchronize(P->gstream);
+        cudaStreamDestroy(P->gstream);
+        cudaEventDestroy(P->gev[0]);
+        cudaEventDestroy(P->gev[1]);
+    }
     free_workspace(P);
     free_table(P);
     delete P;

@@ -242,6 +242,32 @@ __global__ void k_moments_final(const double *partial, int nblocks, double scale
     }
 }
 
+// moments row selected by a device counter (graph-replayable): out[ctr] = ..., ctr++
+__global__ void k_moments_final_ctr(const double *partial, int nblocks, double scale, double *base, int *ctr)
+{
+    constexpr int K = kMaxD + 2;
+    const int row = *ctr;
+    if (threadIdx.x < K) {
+        double s = 0.0;
+        for (int b = 0; b < nblocks; ++b) s += partial[b * K + threadIdx.x];
+        base[(size_t)row * K + threadIdx.x] = s * scale;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *ctr = row + 1;
+}
+
+// TVD-RK2 (Heun) stages: f1 = f + dt q ; f = (f + f1 + dt q1) / 2
+__global__ void k_rk2_stage1(const double *f, const double *q, double dt, double *f1, int64_t n)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        f1[i] = f[i] + dt * q[i];
+}
+__global__ void k_rk2_stage2(double *f, const double *f1, const double *q1, double dt, int64_t n)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        f[i] = 0.5 * (f[i] + (f1[i] + dt * q1[i]));
+}
+
 __global__ void k_axpy(double *f, const double *q, double dt, int64_t n)
 {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -313,7 +339,10 @@ dvm_status_t collide_batched(dvm_plan_s *P, const double *f, double *Q, int64_t 
 {
     const Geo g = geo_of(P);
     if (ncells == 0) return DVM_OK;
-    if (!P->force_v1) {
+    // auto: the 3D frame-plane kernel when built; the 2D pair kernels from
+    // N = 128 (below, the v1 sweeps are faster: fewer, latency-bound launches)
+    const bool use_new = P->path_mode == 2 || (P->path_mode == 0 && (P->d == 3 || P->N >= 128));
+    if (use_new) {
         bool handled = false;
         dvm_status_t st = P->d == 3 ? collide_gain3d(P, f, stride, Q, stride, ncells, &handled)
                                     : collide_pair2d(P, f, stride, Q, stride, ncells, &handled);
@@ -389,6 +418,38 @@ dvm_status_t moments(dvm_plan_s *P, const double *f, double *dev_out_row)
     return DVM_OK;
 }
 
+dvm_status_t moments_ctr(dvm_plan_s *P, const double *f, double *dev_base, int *dev_ctr)
+{
+    const Geo g = geo_of(P);
+    if (!P->ws.mom_partial) DVM_CUDA(cudaMalloc(&P->ws.mom_partial, sizeof(double) * kMomBlocks * (kMaxD + 2)));
+    double scale = 1.0;
+    for (int j = 0; j < P->d; ++j) scale *= P->h;
+    {
+        LaunchScope ls(P, KC_MOMENTS);
+        k_moments_partial<<<kMomBlocks, kThreads, 0, P->stream>>>(f, g, P->h, P->ws.mom_partial);
+    }
+    {
+        LaunchScope ls(P, KC_MOMENTS);
+        k_moments_final_ctr<<<1, 32, 0, P->stream>>>(P->ws.mom_partial, kMomBlocks, scale, dev_base, dev_ctr);
+    }
+    DVM_CUDA(cudaGetLastError());
+    return DVM_OK;
+}
+
+dvm_status_t rk2_stage(dvm_plan_s *P, int stage, double *f, double *f1, const double *q, double dt)
+{
+    const Geo g = geo_of(P);
+    {
+        LaunchScope ls(P, KC_AXPY);
+        if (stage == 1)
+            k_rk2_stage1<<<296, kThreads, 0, P->stream>>>(f, q, dt, f1, g.nodes);
+        else
+            k_rk2_stage2<<<296, kThreads, 0, P->stream>>>(f, f1, q, dt, g.nodes);
+    }
+    DVM_CUDA(cudaGetLastError());
+    return DVM_OK;
+}
+
 dvm_status_t axpy(dvm_plan_s *P, double *f, const double *q, double dt)
 {
     const Geo g = geo_of(P);
@@ -413,7 +474,7 @@ void free_workspace(dvm_plan_s *P)
 {
     clear_profile(P);
     Workspace &w = P->ws;
-    void *ptrs[] = {w.S, w.part, w.f_stage, w.q_stage, w.mom_partial, w.mom_dev, w.qtmp, w.fft_z, w.g3_f, w.g3_t, w.g3_q, w.g3_ctr, w.p2_scr, w.p2_part};
+    void *ptrs[] = {w.S, w.part, w.f_stage, w.q_stage, w.mom_partial, w.mom_dev, w.qtmp, w.f1tmp, w.mom_ctr, w.fft_z, w.g3_f, w.g3_t, w.g3_q, w.g3_ctr, w.p2_scr, w.p2_part};
     for (void *q : ptrs)
         if (q) cudaFree(q);
     w = Workspace{};

@@ -68,7 +68,9 @@ struct Workspace {
     double *mom_partial = nullptr;  // [kMomBlocks][kMaxD+2]
     double *mom_dev = nullptr;      // [(steps+1)][kMaxD+2]
     size_t mom_rows = 0;
-    double *qtmp = nullptr;         // euler scratch (nodes)
+    double *qtmp = nullptr;         // time stepping scratch: Q (nodes)
+    double *f1tmp = nullptr;        // time stepping scratch: RK2 first stage (nodes)
+    int *mom_ctr = nullptr;         // time stepping: device row counter of the moments table
     double2 *fft_z = nullptr;       // 3D loss: complex FFT workspace [pairs][nodes]
     double2 *g3_f = nullptr;        // 3D gain: cell pairs of f, interleaved [pairs][nodes]
     double2 *g3_t = nullptr;        // 3D gain: per-group ring of T_e buffers [groups][slots][nodes]
@@ -125,7 +127,10 @@ struct dvm_plan_s {
     uint64_t launches = 0;
     size_t table_bytes = 0;
     bool profiling = false;
-    bool force_v1 = false;  // evaluation path selector (testing): v1 orbit sweeps only
+    int path_mode = 0;      // evaluation path: 0 auto, 1 v1 orbit sweeps, 2 gain3d/pair2d when built
+    bool use_graphs = true; // time steppers replay one captured step (CUDA graph)
+    cudaStream_t gstream = nullptr;      // plan-owned stream for graph capture/replay
+    cudaEvent_t gev[2] = {nullptr, nullptr};
     std::vector<dvm::ProfRec> prof;
 };
 
@@ -197,6 +202,8 @@ void free_table(dvm_plan_s *P);
 dvm_status_t collide_batched(dvm_plan_s *P, const double *f, double *Q, int64_t ncells, int64_t stride);
 dvm_status_t moments(dvm_plan_s *P, const double *f, double *dev_out_row);
 dvm_status_t axpy(dvm_plan_s *P, double *f, const double *q, double dt);
+dvm_status_t moments_ctr(dvm_plan_s *P, const double *f, double *dev_base, int *dev_ctr);
+dvm_status_t rk2_stage(dvm_plan_s *P, int stage, double *f, double *f1, const double *q, double dt);
 dvm_status_t zero_cells(dvm_plan_s *P, double *Q, int64_t q_stride, int64_t ncells, int64_t nodes);
 dvm_status_t reduce_slots(dvm_plan_s *P, double *Q, int64_t q_stride, const double *part, int64_t slot_elems,
                           int nslots, int64_t ncells, int64_t nodes);

@@ -69,6 +69,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "dvm_collide_batched_host": ([P, V, V, I64, I64], ctypes.c_int),
         "dvm_moments": ([P, V, V], ctypes.c_int),
         "dvm_euler": ([P, V, D, ctypes.c_int, V], ctypes.c_int),
+        "dvm_rk2": ([P, V, D, ctypes.c_int, V], ctypes.c_int),
+        "dvm_set_graphs": ([P, ctypes.c_int], ctypes.c_int),
         "dvm_sync": ([P], ctypes.c_int),
         "dvm_plan_destroy": ([P], ctypes.c_int),
         "dvm_status_str": ([ctypes.c_int], ctypes.c_char_p),
@@ -224,6 +226,18 @@ class Plan:
         _check(lib.dvm_euler(self._h, _dptr(f), float(dt), int(nsteps),
                              mom.ctypes.data if mom is not None else None), "dvm_euler")
         return mom
+
+    def rk2(self, f, dt: float, nsteps: int, moments: bool = True):
+        """In-place TVD-RK2 (Heun) steps (one cell); returns moments [nsteps+1, d+2]."""
+        lib = self._prep_inplace(f)
+        mom = np.zeros((nsteps + 1, self.d + 2), dtype=np.float64) if moments else None
+        _check(lib.dvm_rk2(self._h, _dptr(f), float(dt), int(nsteps),
+                           mom.ctypes.data if mom is not None else None), "dvm_rk2")
+        return mom
+
+    def set_graphs(self, enable: bool):
+        """Enable/disable the CUDA-graph replay of the time steppers."""
+        _check(load().dvm_set_graphs(self._h, 1 if enable else 0), "dvm_set_graphs")
 
     def set_path(self, path: int):
         """0 = default kernels, 1 = v1 orbit sweeps (cross-check path)."""

@@ -215,6 +215,7 @@ def test_c2_euler_trajectory():
 @pytest.mark.parametrize("d,N,Nbar", [(2, 64, 8), (3, 32, 4)])
 def test_constant_field(d, N, Nbar):
     p = _plan(d, N, Nbar)
+    p.set_path(2)  # the FFT-loss path
     Q1 = _gpu(p, np.ones(N ** d))
     # the loss is an FFT convolution: exact only up to rounding (reading R18) ...
     _, G1, _ = oracle.collide(np.ones(N ** d), d, N, Nbar, p.Ntilde, 8.0, points=np.arange(4))
@@ -336,6 +337,7 @@ def test_pair2d_path_matches_orbit_path(N, Nbar, Nt, cells):
     oracle parity on sampled nodes."""
     f = np.random.default_rng(N + cells).uniform(0.0, 1.0, size=(cells, N ** 2))
     p = _plan(2, N, Nbar, Ntilde=Nt)
+    p.set_path(2)  # the pair kernels also below the auto threshold
     q2 = _gpu(p, f)
     p.set_path(1)
     q1 = _gpu(p, f)
@@ -343,3 +345,44 @@ def test_pair2d_path_matches_orbit_path(N, Nbar, Nt, cells):
     pts = np.arange(0, N ** 2, max(1, N ** 2 // 157))
     Qo, _, _ = oracle.collide(f[-1], 2, N, Nbar, Nt, 8.0, points=pts)
     _assert_parity(q2[-1][pts], Qo[0], f"pair2d N={N}", ref=np.abs(q1[-1]).max())
+
+
+# ---------------------------------------------------------------- time steppers (CUDA graphs)
+@pytest.mark.parametrize("d,N,Nbar,Nt,path", [(2, 64, 8, 14, 0), (2, 64, 8, 14, 2), (3, 32, 2, 5, 0)])
+def test_stepper_graph_replay_is_bitwise(d, N, Nbar, Nt, path):
+    """Steps 2..n replay one captured CUDA graph: identical bits and moments to
+    direct launches, for Euler and RK2 (v1, pair2d + FFT loss, gain3d)."""
+    f0 = dvm_inputs.two_bumps(d, N, 8.0, 1.0, 0.01, 4).reshape(-1)
+    p = _plan(d, N, Nbar, Ntilde=Nt)
+    p.set_path(path)
+    for method in ("euler", "rk2"):
+        out = []
+        for graphs in (True, False):
+            p.set_graphs(graphs)
+            f = torch.from_numpy(f0.copy()).cuda()
+            m = getattr(p, method)(f, 0.01, 6)
+            out.append((f.cpu().numpy(), m))
+        assert np.array_equal(out[0][0], out[1][0]), method
+        assert np.array_equal(out[0][1], out[1][1]), method
+    p.set_graphs(True)
+
+
+def test_rk2_matches_oracle_heun():
+    """TVD-RK2 (Heun) on c1 for 3 steps against the same
+    scheme evaluated with the CPU oracle."""
+    cfg = dvm_inputs.CONFIGS["c1"]
+    f0 = dvm_inputs.make("c1")[0]
+    p = _plan(2, cfg.N, cfg.Nbar)
+    dt = 0.05
+    f = torch.from_numpy(f0.copy()).cuda()
+    m = p.rk2(f, dt, 3)
+    fo = f0.copy()
+    for _ in range(3):
+        q0 = oracle.collide(fo, 2, cfg.N, cfg.Nbar, p.Ntilde, cfg.L)[0].reshape(-1)
+        f1 = fo + dt * q0
+        q1 = oracle.collide(f1, 2, cfg.N, cfg.Nbar, p.Ntilde, cfg.L)[0].reshape(-1)
+        fo = 0.5 * (fo + (f1 + dt * q1))
+    fg = f.cpu().numpy()
+    assert np.abs(fg - fo).max() <= 1e-13 * np.abs(fo).max()
+    # mass exactly conserved by every stage (PAPER.md:859-865)
+    assert np.all(np.abs(m[:, 0] - m[0, 0]) <= 1e-13 * m[0, 0])
