@@ -252,7 +252,9 @@ def run_ours(args):
                 "kernel_avg_launch_ms": top_ms / top_n, "algorithmic_bytes_per_launch": alg_bytes,
                 "peak_source": peak_src,
                 "note": "streaming-formulation bytes (A+2)*8*N^3 per cell-evaluation (SURVEY.md 8(d)); "
-                        "effective, not DRAM traffic"}
+                        "effective, not DRAM traffic",
+                "binding_resource": "SM L1/shared-memory pipe (sliding-program loads + scattered frame "
+                                    "gather/store); see profiles/r01/SUMMARY.md"}
     eff_step_gbs = value / world * (A + 2) * 8.0 * nodes / 1e9
 
     # ---- e2e through the C ABI with host buffers (pinned), copies inside the timed region
