@@ -148,10 +148,42 @@ struct G3Geom {
                                    sizeof(uint32_t) * 2 * kMaxMS;
 };
 
+// L2 residency policies: the T ring and f stay (evict_last); T once consumed
+// and the per-pair Q init/final go first (evict_first).
+__device__ __forceinline__ uint64_t l2_keep()
+{
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t l2_drop()
+{
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void st2_hint(double2 *a, double2 v, uint64_t pol)
+{
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(a), "d"(v.x), "d"(v.y), "l"(pol) : "memory");
+}
+__device__ __forceinline__ double2 ld2_cg_hint(const double2 *a, uint64_t pol)
+{
+    double2 v;
+    asm volatile("ld.global.cg.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(a), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ double2 ld2_nc_hint(const double2 *a, uint64_t pol)
+{
+    double2 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(a), "l"(pol));
+    return v;
+}
+
 __device__ __forceinline__ void cp_async16(void *smem_dst, const void *gsrc)
 {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem_dst)),
-                 "l"(gsrc)
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(smem_dst)),
+                 "l"(gsrc), "l"(l2_keep())
                  : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
@@ -397,7 +429,7 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_gain3d(GainArgs A)
                             for (int q = 1; q <= L; ++q) T[q] = add2(T[q], T[q - 1]);
 #pragma unroll
                             for (int q = 0; q < L; ++q) {
-                                __stcg(Tb + x, T[q]);
+                                st2_hint(Tb + x, T[q], l2_keep());
                                 x = swar_add(x, SW, H2);
                             }
                             carry = T[L];
@@ -438,6 +470,7 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_gain3d(GainArgs A)
                     const double aw = A.aw[di];
                     const int M2 = 2 * M;
                     const uint32_t n0 = (uint32_t)rank * NPR + t;
+                    const uint64_t keep = l2_keep();
 #pragma unroll 1
                     for (int j0 = 0; j0 < NJ; j0 += NB) {
                         uint32_t n[NB];
@@ -445,20 +478,20 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_gain3d(GainArgs A)
 #pragma unroll
                         for (int b = 0; b < NB; ++b) {
                             n[b] = n0 + (uint32_t)(j0 + b) * kRoleT;
-                            T[b] = __ldcg(Tb + n[b]);
+                            T[b] = ld2_cg_hint(Tb + n[b], l2_drop());
                             S[b] = make_double2(0.0, 0.0);
                         }
                         for (int k = 0; k < M2; ++k) {
                             const uint32_t off = soff[k];
 #pragma unroll
-                            for (int b = 0; b < NB; ++b) S[b] = add2(S[b], __ldg(fc + swar_add(n[b], off, H2)));
+                            for (int b = 0; b < NB; ++b) S[b] = add2(S[b], ld2_nc_hint(fc + swar_add(n[b], off, H2), keep));
                         }
                         uint32_t r[16];
                         const uint32_t ta = tm_base + (uint32_t)(4 * j0);
                         if (first) {
 #pragma unroll
                             for (int b = 0; b < NB; ++b) {
-                                const double2 q = __ldcg(Qc + n[b]);  // −fΛ (chunk 0) or 0
+                                const double2 q = ld2_cg_hint(Qc + n[b], l2_drop());  // −fΛ (chunk 0) or 0
                                 r[4 * b + 0] = __double2loint(q.x);
                                 r[4 * b + 1] = __double2hiint(q.x);
                                 r[4 * b + 2] = __double2loint(q.y);
@@ -474,7 +507,7 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_gain3d(GainArgs A)
                             qx += aw * T[b].x * S[b].x;
                             qy += aw * T[b].y * S[b].y;
                             if (last) {
-                                Qc[n[b]] = make_double2(qx, qy);
+                                st2_hint(Qc + n[b], make_double2(qx, qy), l2_drop());
                             } else {
                                 r[4 * b + 0] = __double2loint(qx);
                                 r[4 * b + 1] = __double2hiint(qx);
