@@ -148,6 +148,13 @@ DVM_API dvm_status_t dvm_collide_batched_host(dvm_plan_t plan, const double *f_h
  * deterministic. */
 DVM_API dvm_status_t dvm_moments(dvm_plan_t plan, const double *f, double *out_host);
 
+/* dst cell dst_idx[c] = src cell src_idx[c] for c < ncells (cells of N^d
+ * doubles, device arrays; device int64 index arrays, NULL = identity; no range
+ * checks on the indices).  Stream-ordered, asynchronous.  Used to bucket the
+ * cells of a batch by N̄ (space-dependent N̄). */
+DVM_API dvm_status_t dvm_copy_cells(dvm_plan_t plan, const double *src, const int64_t *src_idx, double *dst,
+                                    const int64_t *dst_idx, int64_t ncells);
+
 /* Explicit Euler f <- f + dt D(f,f), nsteps times, in place on the device
  * array f (one cell).  If moments_host != NULL it receives (nsteps+1) rows of
  * d+2 moments (before the first step and after every step).  Synchronous. */

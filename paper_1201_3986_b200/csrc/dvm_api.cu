@@ -462,6 +462,20 @@ static dvm_status_t time_stepper(dvm_plan_s *P, int scheme, double *f, double dt
     return DVM_OK;
 }
 
+dvm_status_t dvm_copy_cells(dvm_plan_t P, const double *src, const int64_t *src_idx, double *dst,
+                            const int64_t *dst_idx, int64_t ncells)
+{
+    if (!P || !src || !dst) {
+        set_error("NULL argument");
+        return DVM_E_NULL;
+    }
+    if (ncells < 0) {
+        set_error("ncells < 0");
+        return DVM_E_SHAPE;
+    }
+    return copy_cells(P, src, src_idx, dst, dst_idx, ncells);
+}
+
 dvm_status_t dvm_euler(dvm_plan_t P, double *f, double dt, int nsteps, double *moments_host)
 {
     return time_stepper(P, 1, f, dt, nsteps, moments_host);

@@ -256,6 +256,18 @@ __global__ void k_moments_final_ctr(const double *partial, int nblocks, double s
     if (threadIdx.x == 0) *ctr = row + 1;
 }
 
+// dst[dst_idx[c]] = src[src_idx[c]] for c < ncells (NULL index = identity), one cell = nodes doubles
+__global__ void k_copy_cells(const double *__restrict__ src, const int64_t *__restrict__ si, double *__restrict__ dst,
+                             const int64_t *__restrict__ di, int64_t ncells, int64_t nodes)
+{
+    const int64_t total = ncells * nodes;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = i / nodes, x = i % nodes;
+        const int64_t a = si ? si[c] : c, b = di ? di[c] : c;
+        dst[b * nodes + x] = src[a * nodes + x];
+    }
+}
+
 // TVD-RK2 (Heun) stages: f1 = f + dt q ; f = (f + f1 + dt q1) / 2
 __global__ void k_rk2_stage1(const double *f, const double *q, double dt, double *f1, int64_t n)
 {
@@ -431,6 +443,19 @@ dvm_status_t moments_ctr(dvm_plan_s *P, const double *f, double *dev_base, int *
     {
         LaunchScope ls(P, KC_MOMENTS);
         k_moments_final_ctr<<<1, 32, 0, P->stream>>>(P->ws.mom_partial, kMomBlocks, scale, dev_base, dev_ctr);
+    }
+    DVM_CUDA(cudaGetLastError());
+    return DVM_OK;
+}
+
+dvm_status_t copy_cells(dvm_plan_s *P, const double *src, const int64_t *si, double *dst, const int64_t *di,
+                        int64_t ncells)
+{
+    const Geo g = geo_of(P);
+    if (ncells <= 0) return DVM_OK;
+    {
+        LaunchScope ls(P, KC_ZERO);
+        k_copy_cells<<<592, kThreads, 0, P->stream>>>(src, si, dst, di, ncells, g.nodes);
     }
     DVM_CUDA(cudaGetLastError());
     return DVM_OK;

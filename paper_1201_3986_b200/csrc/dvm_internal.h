@@ -204,6 +204,8 @@ dvm_status_t moments(dvm_plan_s *P, const double *f, double *dev_out_row);
 dvm_status_t axpy(dvm_plan_s *P, double *f, const double *q, double dt);
 dvm_status_t moments_ctr(dvm_plan_s *P, const double *f, double *dev_base, int *dev_ctr);
 dvm_status_t rk2_stage(dvm_plan_s *P, int stage, double *f, double *f1, const double *q, double dt);
+dvm_status_t copy_cells(dvm_plan_s *P, const double *src, const int64_t *si, double *dst, const int64_t *di,
+                        int64_t ncells);
 dvm_status_t zero_cells(dvm_plan_s *P, double *Q, int64_t q_stride, int64_t ncells, int64_t nodes);
 dvm_status_t reduce_slots(dvm_plan_s *P, double *Q, int64_t q_stride, const double *part, int64_t slot_elems,
                           int nslots, int64_t ncells, int64_t nodes);

@@ -70,6 +70,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "dvm_moments": ([P, V, V], ctypes.c_int),
         "dvm_euler": ([P, V, D, ctypes.c_int, V], ctypes.c_int),
         "dvm_rk2": ([P, V, D, ctypes.c_int, V], ctypes.c_int),
+        "dvm_copy_cells": ([P, V, V, V, V, I64], ctypes.c_int),
         "dvm_set_graphs": ([P, ctypes.c_int], ctypes.c_int),
         "dvm_sync": ([P], ctypes.c_int),
         "dvm_plan_destroy": ([P], ctypes.c_int),
@@ -234,6 +235,14 @@ class Plan:
         _check(lib.dvm_rk2(self._h, _dptr(f), float(dt), int(nsteps),
                            mom.ctypes.data if mom is not None else None), "dvm_rk2")
         return mom
+
+    def copy_cells(self, src, src_idx, dst, dst_idx, ncells: int):
+        """dst[dst_idx[c]] = src[src_idx[c]] (CUDA float64 cells, CUDA int64 indices or None)."""
+        lib = load()
+        _check(lib.dvm_set_stream(self._h, _stream_ptr()), "dvm_set_stream")
+        _check(lib.dvm_copy_cells(self._h, _dptr(src), _dptr(src_idx) if src_idx is not None else None,
+                                  _dptr(dst), _dptr(dst_idx) if dst_idx is not None else None, int(ncells)),
+               "dvm_copy_cells")
 
     def set_graphs(self, enable: bool):
         """Enable/disable the CUDA-graph replay of the time steppers."""

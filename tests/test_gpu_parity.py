@@ -386,3 +386,27 @@ def test_rk2_matches_oracle_heun():
     assert np.abs(fg - fo).max() <= 1e-13 * np.abs(fo).max()
     # mass exactly conserved by every stage
     assert np.all(np.abs(m[:, 0] - m[0, 0]) <= 1e-13 * m[0, 0])
+
+
+# ---------------------------------------------------------------- space-dependent N̄
+def test_adaptive_nbar_buckets():
+    """Cells evaluated at their own N̄ (shared Ñ) through bucketing equal the
+    single-level evaluation of each cell, and the oracle on sampled nodes."""
+    from paper_1201_3986_b200.adaptive import AdaptiveNbar, equilibrium_levels
+    d, N = 3, 32
+    ad = AdaptiveNbar(d, N, [1, 2, 4])
+    f = np.stack([dvm_inputs.two_bumps(d, N, 8.0, 0.5 + 0.3 * c, 0.02, c).reshape(-1) for c in range(6)])
+    nb = np.array([4, 1, 2, 4, 1, 2])
+    ft = torch.from_numpy(f).cuda()
+    q = ad.collide(ft, nb).cpu().numpy()
+    for c in range(6):
+        q1 = ad.plans[int(nb[c])].collide(ft[c].contiguous()).cpu().numpy()
+        np.testing.assert_allclose(q[c], q1, rtol=0, atol=1e-13 * np.abs(q1).max())
+    pts = np.arange(0, N ** 3, 997)
+    for c in (1, 2, 3):
+        Qo, _, _ = oracle.collide(f[c], d, N, int(nb[c]), ad.Ntilde, 8.0, points=pts)
+        _assert_parity(q[c][pts], Qo[0], f"adaptive cell {c} N̄={nb[c]}")
+    # the reference policy: a Maxwellian cell gets the lowest level
+    m = dvm_inputs.make("c5", cells=2)
+    lv, delta = equilibrium_levels(torch.from_numpy(m).cuda(), 3, 64, 8.0, [2, 8], [0.05])
+    assert lv.shape == (2,) and np.all(delta < 0.05) and np.all(lv == 2)
