@@ -566,8 +566,9 @@ size_t gain_smem_bytes(int N) { return N == 32 ? G3Geom<32>::smem : G3Geom<64>::
 
 template <int N>
 dvm_status_t launch_gain(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q, int64_t q_stride,
-                         int64_t ncells)
+                         int64_t ncells, bool *fallback)
 {
+    *fallback = false;
     auto kern = k_gain3d<N>;
     const size_t smem = gain_smem_bytes(N);
     DVM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -576,9 +577,9 @@ dvm_status_t launch_gain(dvm_plan_s *P, const double *f, int64_t f_stride, doubl
     DVM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     DVM_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
     DVM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 2 * kRoleT, smem));
-    if (!coop || per_sm < 1) {
-        set_error("gain3d kernel cannot be launched cooperatively on this device");
-        return DVM_E_CUDA;
+    if (!coop || per_sm < 1) {  // no cooperative launch here: the v1 sweeps evaluate
+        *fallback = true;
+        return DVM_OK;
     }
     int max_groups = (sms * per_sm) / kCL;
     if (getenv("DVM_G3_GROUPS")) max_groups = std::max(1, std::min(max_groups, atoi(getenv("DVM_G3_GROUPS"))));
@@ -626,7 +627,16 @@ dvm_status_t launch_gain(dvm_plan_s *P, const double *f, int64_t f_stride, doubl
     {
         void *args[] = {&a};
         LaunchScope ls(P, KC_GAIN3D);
-        DVM_CUDA(cudaLaunchCooperativeKernel((void *)kern, dim3(ngroups * kCL), dim3(2 * kRoleT), args, smem, P->stream));
+        const cudaError_t le =
+            cudaLaunchCooperativeKernel((void *)kern, dim3(ngroups * kCL), dim3(2 * kRoleT), args, smem, P->stream);
+        if (le == cudaErrorCooperativeLaunchTooLarge || le == cudaErrorNotSupported) {
+            // the co-residency the group barriers need is not available now (e.g.
+            // SMs held by another context): evaluate with the v1 sweeps instead
+            cudaGetLastError();
+            *fallback = true;
+            return DVM_OK;
+        }
+        if (le != cudaSuccess) return cuda_fail(le, "cudaLaunchCooperativeKernel(k_gain3d)");
     }
     {
         LaunchScope ls(P, KC_REDUCE);
@@ -727,8 +737,18 @@ dvm_status_t collide_gain3d(dvm_plan_s *P, const double *f, int64_t f_stride, do
     if (P->d != 3 || !P->g.ready || ncells <= 0) return DVM_OK;
     *handled = true;
     switch (P->N) {
-    case 32: return launch_gain<32>(P, f, f_stride, Q, q_stride, ncells);
-    case 64: return launch_gain<64>(P, f, f_stride, Q, q_stride, ncells);
+    case 32: {
+        bool fb = false;
+        const dvm_status_t st = launch_gain<32>(P, f, f_stride, Q, q_stride, ncells, &fb);
+        *handled = !fb;
+        return st;
+    }
+    case 64: {
+        bool fb = false;
+        const dvm_status_t st = launch_gain<64>(P, f, f_stride, Q, q_stride, ncells, &fb);
+        *handled = !fb;
+        return st;
+    }
     default: *handled = false; return DVM_OK;
     }
 }

@@ -118,7 +118,6 @@ struct dvm_plan_s {
     dvm::DirTable t;
     // host mirrors (small)
     std::vector<int> h_e, h_M, h_nrows, h_row_off, h_cost;
-    int h_row_extent = -1;  // max over rows of max(|lo-1|, |hi|) (plane-kernel halo check)
     std::vector<double> h_a;
     std::vector<int> local;      // direction indices evaluated by this plan, ascending
     std::vector<uint8_t> is_local;

@@ -414,15 +414,6 @@ dvm_status_t build_table(dvm_plan_s *P)
     DVM_CUDA(cudaMemcpyAsync(P->h_row_off.data(), t.row_off, sizeof(int) * (A + 1), cudaMemcpyDeviceToHost,
                              P->stream));
     DVM_CUDA(cudaMemcpyAsync(P->h_cost.data(), t.cost, sizeof(int) * A, cudaMemcpyDeviceToHost, P->stream));
-    {
-        std::vector<int> lo(R), hi(R);
-        DVM_CUDA(cudaMemcpyAsync(lo.data(), t.row_lo, sizeof(int) * R, cudaMemcpyDeviceToHost, P->stream));
-        DVM_CUDA(cudaMemcpyAsync(hi.data(), t.row_hi, sizeof(int) * R, cudaMemcpyDeviceToHost, P->stream));
-        DVM_CUDA(cudaStreamSynchronize(P->stream));
-        int ext = 0;
-        for (int k = 0; k < R; ++k) ext = std::max(ext, std::max(std::abs(lo[k] - 1), std::abs(hi[k])));
-        P->h_row_extent = ext;
-    }
     P->table_bytes = acc;
 
     // Direction sharding (the decomposition eq:decD is a sum
