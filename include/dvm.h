@@ -182,7 +182,10 @@ DVM_API dvm_status_t dvm_profile_read(dvm_plan_t plan, double *ms, uint64_t *cou
 DVM_API const char *dvm_profile_name(int k);
 
 /* Evaluation path: 0 = auto (default), 1 = v1 orbit sweeps only, 2 = the
- * FFT-loss paths whenever the plan built them.  The FFT-loss paths evaluate
+ * FFT-loss paths whenever the plan built them, 3 = the spectral reference
+ * path (per direction one inverse transform gives
+ * S_e + i T_e from the real filter spectra; a second cross-check, slow:
+ * A inverse FFTs per cell; its tables need 16 A N^d bytes, <= 4 GB).  The FFT-loss paths evaluate
  * the loss as one FFT convolution f (λ ⊛ f) (reading R21): 3D with N in
  * {32, 64}: gain by the frame-plane kernel (two cells per node,
  * warp-specialised, TMEM accumulators); 2D with 16 <= N <= 256: gain by

@@ -353,6 +353,7 @@ dvm_status_t collide_batched(dvm_plan_s *P, const double *f, double *Q, int64_t 
     if (ncells == 0) return DVM_OK;
     // auto: the 3D frame-plane kernel when built; the 2D pair kernels from
     // N = 128 (below, the v1 sweeps are faster: fewer, latency-bound launches)
+    if (P->path_mode == 3) return collide_spectral(P, f, stride, Q, stride, ncells);
     const bool use_new = P->path_mode == 2 || (P->path_mode == 0 && (P->d == 3 || P->N >= 128));
     if (use_new) {
         bool handled = false;
@@ -499,7 +500,7 @@ void free_workspace(dvm_plan_s *P)
 {
     clear_profile(P);
     Workspace &w = P->ws;
-    void *ptrs[] = {w.S, w.part, w.f_stage, w.q_stage, w.mom_partial, w.mom_dev, w.qtmp, w.f1tmp, w.mom_ctr, w.fft_z, w.g3_f, w.g3_t, w.g3_q, w.g3_ctr, w.p2_scr, w.p2_part};
+    void *ptrs[] = {w.S, w.part, w.f_stage, w.q_stage, w.mom_partial, w.mom_dev, w.qtmp, w.f1tmp, w.mom_ctr, w.fft_z, w.g3_f, w.g3_t, w.g3_q, w.g3_ctr, w.p2_scr, w.p2_part, w.sp_z};
     for (void *q : ptrs)
         if (q) cudaFree(q);
     w = Workspace{};

@@ -724,7 +724,7 @@ dvm_status_t build_gain3d(dvm_plan_s *P)
 void free_gain3d(dvm_plan_s *P)
 {
     GainTables &g = P->g;
-    void *ptrs[] = {g.rec, g.aw, g.tw, g.lamhat, g.units};
+    void *ptrs[] = {g.rec, g.aw, g.tw, g.lamhat, g.units, g.shat, g.that};
     for (void *q : ptrs)
         if (q) cudaFree(q);
     g = GainTables{};

@@ -80,6 +80,8 @@ struct Workspace {
     double *p2_scr = nullptr;       // 2D pair path: line windows of the first direction [units][cells][nodes]
     double *p2_part = nullptr;      // 2D pair path: partial gains [units][cells][nodes]
     size_t p2_scr_elems = 0, p2_part_elems = 0;
+    double2 *sp_z = nullptr;        // spectral path: f̂ and the per-direction transform
+    size_t sp_z_elems = 0;
 };
 
 }  // namespace dvm
@@ -104,6 +106,8 @@ struct GainTables {
     void *units = nullptr;    // 2D: direction-pair units (dvm_pair2d.cu)
     int nunits = 0;
     int maxitems2d = 0;       // 2D: work items of the longest line walk
+    double *shat = nullptr;   // spectral path: [A_local][N^d] line-filter spectra (real)
+    double *that = nullptr;   // spectral path: [A_local][N^d] perp-filter spectra (real)
     size_t bytes = 0;
 };
 }  // namespace dvm
@@ -126,7 +130,7 @@ struct dvm_plan_s {
     uint64_t launches = 0;
     size_t table_bytes = 0;
     bool profiling = false;
-    int path_mode = 0;      // evaluation path: 0 auto, 1 v1 orbit sweeps, 2 gain3d/pair2d when built
+    int path_mode = 0;      // evaluation path: 0 auto, 1 v1 orbit sweeps, 2 gain3d/pair2d when built, 3 spectral
     bool use_graphs = true; // time steppers replay one captured step (CUDA graph)
     cudaStream_t gstream = nullptr;      // plan-owned stream for graph capture/replay
     cudaEvent_t gev[2] = {nullptr, nullptr};
@@ -212,6 +216,8 @@ dvm_status_t reduce_slots(dvm_plan_s *P, double *Q, int64_t q_stride, const doub
 dvm_status_t build_loss(dvm_plan_s *P);
 dvm_status_t loss_init(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q, int64_t q_stride, int64_t ncells,
                        double2 *QI);
+dvm_status_t collide_spectral(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q, int64_t q_stride,
+                              int64_t ncells);
 dvm_status_t build_gain3d(dvm_plan_s *P);
 dvm_status_t build_pair2d(dvm_plan_s *P);
 dvm_status_t collide_pair2d(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q, int64_t q_stride,

@@ -212,6 +212,78 @@ dvm_status_t fft_dispatch(dvm_plan_s *P, const FftArgs &a)
     }
 }
 
+// ---------------------------------------------------------------- spectral reference path
+// (dvm_set_path(3); the paper's per-direction spectral evaluation, PAPER.md:
+// 561-570, 816-819): S_e = IFFT(f̂ ŝ_e), T_e = IFFT(f̂ t̂_e) from one complex
+// transform, S_e + i T_e = IFFT(f̂ (ŝ_e + i t̂_e)); Q += a_e S_e T_e on top of −fΛ.
+// ŝ_e(ξ) = Σ_{1<=|m|<=M_e} cos(2π m e.ξ / N), t̂_e(ξ) = Σ_{l ∈ P_e} cos(2π l.ξ / N):
+// the line and perp-set filters are even, their spectra real.  Phases are
+// integers mod N: cos values come from one table (identical for every term).
+__global__ void k_spec_tables(int d, int N, int p, int nloc, const int *local, const int *E, const int *M,
+                              const int *U, const int *W, const int *row_off, const int *row_b, const int *row_lo,
+                              const int *row_hi, const double *ctab, double *shat, double *that)
+{
+    int64_t nodes = 1;
+    for (int q = 0; q < d; ++q) nodes *= N;
+    const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= nodes * nloc) return;
+    const int k = (int)(gid / nodes);
+    const int64_t j = gid % nodes;
+    int xi[3] = {0, 0, 0};
+    for (int q = d - 1, sh = 0; q >= 0; --q, sh += p) xi[q] = (int)((j >> sh) & (N - 1));
+    const int di = local[k];
+    auto dot = [&](const int *v) {
+        int s = 0;
+        for (int q = 0; q < d; ++q) s += v[q] * xi[q];
+        s %= N;
+        return s < 0 ? s + N : s;
+    };
+    const int ev = dot(E + 3 * di), m_e = M[di];
+    double sh_ = 0.0;
+    for (int m = 1; m <= m_e; ++m) sh_ += 2.0 * ctab[(m * ev) & (N - 1)];
+    double th = 0.0;
+    if (d == 2) {
+        const int ep[2] = {-E[3 * di + 1], E[3 * di]};
+        int pv = (ep[0] * xi[0] + ep[1] * xi[1]) % N;
+        if (pv < 0) pv += N;
+        for (int n = -m_e; n <= m_e; ++n) th += ctab[((n * pv) % N + N) & (N - 1)];
+    } else {
+        const int uv = dot(U + 3 * di), wv = dot(W + 3 * di);
+        for (int r = row_off[di]; r < row_off[di + 1]; ++r) {
+            const int b = row_b[r];
+            for (int a = row_lo[r]; a <= row_hi[r]; ++a) th += ctab[(((a * uv + b * wv) % N) + N) & (N - 1)];
+        }
+    }
+    shat[(int64_t)k * nodes + j] = sh_;
+    that[(int64_t)k * nodes + j] = th;
+}
+
+__global__ void k_cos_table(int N, double *ctab)
+{
+    const int n = blockIdx.x * blockDim.x + threadIdx.x;
+    if (n < N) ctab[n] = cospi(2.0 * n / N);
+}
+
+// z1 = z0 (ŝ + i t̂)
+__global__ void k_spec_mul(const double2 *__restrict__ z0, const double *__restrict__ sh, const double *__restrict__ th,
+                           double2 *__restrict__ z1, int64_t n)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double2 a = z0[i];
+        const double s = sh[i], t = th[i];
+        z1[i] = make_double2(a.x * s - a.y * t, a.x * t + a.y * s);
+    }
+}
+
+// Q += a (Re z / n)(Im z / n)   (z = unnormalised inverse transform)
+__global__ void k_spec_acc(const double2 *__restrict__ z, double aw, double scale, double *__restrict__ Q, int64_t n)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double2 v = z[i];
+        Q[i] += aw * (v.x * scale) * (v.y * scale);
+    }
+}
+
 }  // namespace
 
 
@@ -316,5 +388,88 @@ dvm_status_t loss_init(dvm_plan_s *P, const double *f, int64_t f_stride, double 
     return DVM_OK;
 }
 
+
+dvm_status_t collide_spectral(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q, int64_t q_stride,
+                              int64_t ncells)
+{
+    const int d = P->d, N = P->N;
+    int64_t nodes = 1;
+    for (int j = 0; j < d; ++j) nodes *= N;
+    const int nloc = (int)P->local.size();
+    GainTables &g = P->g;
+    if (!g.lamhat) {
+        set_error("spectral path needs the FFT loss tables (3D N in {32, 64}, 2D 16 <= N <= 256)");
+        return DVM_E_UNSUPPORTED;
+    }
+    if ((double)nodes * nloc * 16.0 > 4.0e9) {
+        set_error("spectral path tables would exceed 4 GB");
+        return DVM_E_UNSUPPORTED;
+    }
+    dvm_status_t st;
+    Workspace &w = P->ws;
+    if (!g.shat && nloc > 0) {  // lazily, on first use
+        DVM_CUDA(cudaMalloc(&g.shat, sizeof(double) * nodes * nloc));
+        DVM_CUDA(cudaMalloc(&g.that, sizeof(double) * nodes * nloc));
+        double *ctab = nullptr;
+        DVM_CUDA(cudaMalloc(&ctab, sizeof(double) * N));
+        {
+            LaunchScope ls(P, KC_PLAN);
+            k_cos_table<<<(N + 127) / 128, 128, 0, P->stream>>>(N, ctab);
+            const int64_t tot = nodes * nloc;
+            k_spec_tables<<<(unsigned)((tot + 127) / 128), 128, 0, P->stream>>>(
+                d, N, P->p, nloc, P->t.local, P->t.e, P->t.M, P->t.u, P->t.w, P->t.row_off, P->t.row_b,
+                P->t.row_lo, P->t.row_hi, ctab, g.shat, g.that);
+        }
+        DVM_CUDA(cudaGetLastError());
+        DVM_CUDA(cudaStreamSynchronize(P->stream));
+        cudaFree(ctab);
+    }
+    // Q := −f Λ (the loss, one convolution), then the gain direction by direction
+    if ((st = loss_init(P, f, f_stride, Q, q_stride, ncells, nullptr))) return st;
+    if ((st = grow(&w.sp_z, &w.sp_z_elems, (size_t)(2 * nodes), P->stream))) return st;
+    double2 *z0 = w.sp_z, *z1 = w.sp_z + nodes;
+    const double scale = 1.0 / (double)nodes;
+    for (int64_t c = 0; c < ncells; ++c) {
+        for (int k = 0; k < d; ++k) {  // f̂ of this cell
+            FftArgs a = {};
+            a.d = d;
+            a.npairs = 1;
+            a.tw = g.tw;
+            a.r_cells = 1;
+            a.ax = d - 1 - k;
+            a.zin = z0;
+            a.zout = z0;
+            if (k == 0) {
+                a.r0 = f + c * f_stride;
+                a.r_stride = nodes;
+            }
+            if ((st = fft_dispatch(P, a))) return st;
+        }
+        for (int kd = 0; kd < nloc; ++kd) {
+            {
+                LaunchScope ls(P, KC_FFT);
+                k_spec_mul<<<256, 256, 0, P->stream>>>(z0, g.shat + (int64_t)kd * nodes, g.that + (int64_t)kd * nodes,
+                                                     z1, nodes);
+            }
+            for (int k = 0; k < d; ++k) {
+                FftArgs a = {};
+                a.d = d;
+                a.npairs = 1;
+                a.tw = g.tw;
+                a.inverse = 1;
+                a.ax = k;
+                a.zin = z1;
+                a.zout = z1;
+                if ((st = fft_dispatch(P, a))) return st;
+            }
+            {
+                LaunchScope ls(P, KC_FFT);
+                k_spec_acc<<<256, 256, 0, P->stream>>>(z1, P->h_a[P->local[kd]], scale, Q + c * q_stride, nodes);
+            }
+        }
+        DVM_CUDA(cudaGetLastError());
+    }
+    return DVM_OK;
+}
 
 }  // namespace dvm

@@ -410,3 +410,20 @@ def test_adaptive_nbar_buckets():
     m = dvm_inputs.make("c5", cells=2)
     lv, delta = equilibrium_levels(torch.from_numpy(m).cuda(), 3, 64, 8.0, [2, 8], [0.05])
     assert lv.shape == (2,) and np.all(delta < 0.05) and np.all(lv == 2)
+
+
+# ---------------------------------------------------------------- spectral reference path (dvm_set_path(3))
+@pytest.mark.parametrize("d,N,Nbar,Nt,cells", [(2, 16, 4, 4, 1), (2, 64, 8, 14, 2), (3, 32, 2, 5, 1), (3, 32, 4, 7, 2)])
+def test_spectral_path_matches_oracle(d, N, Nbar, Nt, cells):
+    """The paper's per-direction spectral evaluation (S_e + i T_e from one inverse
+    transform of f̂ (ŝ_e + i t̂_e)) against the oracle and the default path."""
+    f = np.stack([dvm_inputs.two_bumps(d, N, 8.0, 1.0 + 0.2 * c, 0.01, c).reshape(-1) for c in range(cells)])
+    p = _plan(d, N, Nbar, Ntilde=Nt)
+    q0 = _gpu(p, f)
+    p.set_path(3)
+    q3 = _gpu(p, f)
+    np.testing.assert_allclose(q3, q0, rtol=0, atol=1e-12 * np.abs(q0).max())
+    pts = np.arange(0, N ** d, max(1, N ** d // 211))
+    for c in range(cells):
+        Qo, _, _ = oracle.collide(f[c], d, N, Nbar, Nt, 8.0, points=pts)
+        _assert_parity(q3[c][pts], Qo[0], f"spectral d={d} N={N} cell {c}")
