@@ -427,3 +427,18 @@ def test_spectral_path_matches_oracle(d, N, Nbar, Nt, cells):
     for c in range(cells):
         Qo, _, _ = oracle.collide(f[c], d, N, Nbar, Nt, 8.0, points=pts)
         _assert_parity(q3[c][pts], Qo[0], f"spectral d={d} N={N} cell {c}")
+
+
+def test_triple_agreement_c1():
+    """GPU (every path) == direct-sum oracle == the paper's pseudo-spectral route
+    (dense β(K,L), oracle/cross.py) on c1."""
+    from oracle import cross
+    cfg = dvm_inputs.CONFIGS["c1"]
+    f = dvm_inputs.make("c1")[0]
+    p = _plan(2, cfg.N, cfg.Nbar)
+    Qo = oracle.collide(f, 2, cfg.N, cfg.Nbar, p.Ntilde, cfg.L)[0].reshape(-1)
+    Qb, _ = cross.dense_beta_Q(f, 2, cfg.N, cfg.Nbar, p.Ntilde, cfg.L)
+    _assert_parity(Qb, Qo, "dense beta vs oracle")
+    for path in (0, 1, 2, 3):
+        p.set_path(path)
+        _assert_parity(_gpu(p, f).reshape(-1), Qb, f"path {path} vs dense beta")

@@ -15,6 +15,11 @@ P10 gain coefficients non-negative: G >= 0 for f >= 0
 P11 direction counts: Fig. 1 (16 lines), A^1 = 4(|F^1|-1) with |F^1| by its
     definition (PAPER.md:600-615), Möbius closed form in 2D/3D, partition property;
     Ñ rule values 1,3,7,14
+P12 the pseudo-spectral route (eq:sysDiff, eq:betaKL): the
+    dense β(K,L) evaluation (oracle/cross.py, its own pair set) equals the oracle
+P13 the box-truncated D^tr (oracle/cross.py) conserves mass,
+    momentum and energy for any f, and equals the periodized operator when no
+    collision of supp f leaves the box
 """
 import itertools
 import math
@@ -364,3 +369,42 @@ def test_ntilde_rule_paper_values():
     assert [oracle.ntilde_rule(N, 1) for N in (8, 16, 32, 64, 128)] == [1, 3, 7, 14, 28]
     # BASELINE configs (reading R2): c1 raises Ñ to N̄ = 4
     assert [oracle.ntilde_rule(N, Nb) for N, Nb in ((16, 4), (64, 8), (256, 16), (32, 4), (64, 8))] == [4, 14, 57, 7, 14]
+
+
+# ---------------------------------------------------------------- P12, P13: cross-oracles
+@pytest.mark.parametrize("d,N,Nb,Nt", [(2, 8, 1, 3), (2, 9, 2, 4), (2, 12, 3, 5), (3, 5, 1, 2), (3, 6, 2, 2)])
+def test_p12_pseudo_spectral_route(d, N, Nb, Nt):
+    from oracle import cross
+    f = np.random.default_rng(N * 10 + d).uniform(0.0, 1.0, N ** d)
+    Qo = oracle.collide(f, d, N, Nb, Nt, 8.0)[0].reshape(-1)
+    Qb, imag = cross.dense_beta_Q(f, d, N, Nb, Nt, 8.0)
+    scale = np.abs(Qo).max()
+    assert np.abs(Qb - Qo).max() <= 1e-13 * scale
+    assert imag <= 1e-13 * scale  # real f: the spectral sum is real
+
+
+@pytest.mark.parametrize("d,N,Nb,Nt", [(2, 12, 2, 3), (3, 7, 1, 2)])
+def test_p13_truncated_operator_conserves_and_matches_interior(d, N, Nb, Nt):
+    from oracle import cross
+    L = 8.0
+    h = 2 * L / N
+    v = (np.arange(N) - N // 2) * h
+    V = np.stack(np.meshgrid(*([v] * d), indexing="ij"), axis=-1).reshape(-1, d)
+    f = np.random.default_rng(2 + d).uniform(0.0, 1.0, N ** d)
+    Dt = cross.D_tr(f, d, N, Nb, Nt, L)
+    scale = np.abs(Dt).sum() * (1 + np.abs(V).max() ** 2)
+    assert abs(Dt.sum()) <= 1e-14 * scale
+    for j in range(d):
+        assert abs((Dt * V[:, j]).sum()) <= 1e-14 * scale
+    assert abs((Dt * (V ** 2).sum(1)).sum()) <= 1e-14 * scale
+    # the periodized operator is not conservative for this f (it wraps) ...
+    Qo = oracle.collide(f, d, N, Nb, Nt, L)[0].reshape(-1)
+    assert abs((Qo * (V ** 2).sum(1)).sum()) > 1e-6 * scale
+    # ... but equals D^tr when every collision of supp f stays in the box
+    g = np.zeros((N,) * d)
+    lo, hi = N // 2 - 1, N // 2 + 1
+    sl = tuple(slice(lo, hi) for _ in range(d))
+    g[sl] = np.random.default_rng(5).uniform(0.5, 1.0, g[sl].shape)
+    Qg = oracle.collide(g.reshape(-1), d, N, Nb, Nt, L)[0].reshape(-1)
+    Dg = cross.D_tr(g.reshape(-1), d, N, Nb, Nt, L)
+    assert np.abs(Dg - Qg).max() <= 1e-13 * np.abs(Qg).max()
