@@ -22,8 +22,10 @@ def _line_order(k):
     return max(abs(c) // g for c in k), g
 
 
-def collide(f: np.ndarray, Nbar: int, Ntilde: int, h: float):
-    """f has shape [N]*d.  Returns Q with the same shape."""
+def collide(f: np.ndarray, Nbar: int, Ntilde: int, h: float, a_box=None, b_box=None):
+    """f has shape [N]*d.  Returns Q with the same shape.  a_box, b_box:
+    optional decoupled weights a(k), b(l) (eq:decoup) as
+    arrays of shape [2Ñ+1]*d indexed by k + Ñ."""
     f = np.asarray(f, dtype=np.float64)
     d = f.ndim
     rng = range(-Ntilde, Ntilde + 1)
@@ -40,10 +42,13 @@ def collide(f: np.ndarray, Nbar: int, Ntilde: int, h: float):
         if order > Nbar:
             continue
         a = h ** (d + 1) * math.sqrt(sum(c * c for c in k)) / g
+        if a_box is not None:
+            a = float(a_box[tuple(c + Ntilde for c in k)])
         fk = shifted(k)
         for l in itertools.product(rng, repeat=d):
             if sum(x * y for x, y in zip(k, l)) != 0:
                 continue
             kl = tuple(x + y for x, y in zip(k, l))
-            Q += a * (fk * shifted(l) - f * shifted(kl))
+            w = a if b_box is None else a * float(b_box[tuple(c + Ntilde for c in l)])
+            Q += w * (fk * shifted(l) - f * shifted(kl))
     return Q

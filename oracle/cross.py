@@ -18,7 +18,8 @@ D_tr          the box-truncated operator of PAPER.md:371-381:
 Both build the truncated pair set from its definition here (no code shared
 with oracle/dvm_oracle.c): k ≠ 0 in [-Ñ,Ñ]^d on a line of order <= N̄
 (|k / gcd(k)|_inf <= N̄), l in [-Ñ,Ñ]^d with k.l = 0, Γ~_{k,l} = a(k) =
-h^{d+1} |k| / gcd(k) (readings R4, R5, R8, R9).
+h^{d+1} |k| / gcd(k) (readings R4, R5, R8, R9), or
+Γ~_{k,l} = a(k) b(l) from caller weight tables (eq:decoup).
 """
 from __future__ import annotations
 
@@ -28,7 +29,7 @@ import math
 import numpy as np
 
 
-def _pairs(d, N, Nbar, Ntilde, L):
+def _pairs(d, N, Nbar, Ntilde, L, a_box=None, b_box=None):
     h = 2.0 * L / N
     box = list(itertools.product(range(-Ntilde, Ntilde + 1), repeat=d))
     K, Lp, A = [], [], []
@@ -41,17 +42,20 @@ def _pairs(d, N, Nbar, Ntilde, L):
         if max(abs(c) for c in k) // g > Nbar:
             continue
         a = h ** (d + 1) * math.sqrt(sum(c * c for c in k)) / g
+        if a_box is not None:  # eq:decoup with caller weights: Γ~ = a(k) b(l)
+            a = float(a_box[tuple(c + Ntilde for c in k)])
         for l in box:
             if sum(x * y for x, y in zip(k, l)) == 0:
                 K.append(k)
                 Lp.append(l)
-                A.append(a)
+                A.append(a if b_box is None else a * float(b_box[tuple(c + Ntilde for c in l)]))
     return np.array(K, dtype=np.int64), np.array(Lp, dtype=np.int64), np.array(A, dtype=np.float64)
 
 
-def dense_beta_Q(f, d, N, Nbar, Ntilde, L=8.0):
-    """Q by the pseudo-spectral route (complex128), real part returned."""
-    k, l, a = _pairs(d, N, Nbar, Ntilde, L)
+def dense_beta_Q(f, d, N, Nbar, Ntilde, L=8.0, a_box=None, b_box=None):
+    """Q by the pseudo-spectral route (complex128), real part returned.
+    a_box, b_box: optional decoupled weights (eq:decoup), [2Ñ+1]*d arrays."""
+    k, l, a = _pairs(d, N, Nbar, Ntilde, L, a_box, b_box)
     grid = np.array(list(itertools.product(range(N), repeat=d)))  # mode index K (row-major)
     n = grid.shape[0]
     # E_k[p, K] = e_K(k_p) = exp(2πi K.k_p / N)

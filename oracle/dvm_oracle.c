@@ -19,6 +19,11 @@
  *
  *   a(k) = h^{d+1} |k|_2 / gcd(|k_1|,...,|k_d|),   b(l) = 1,    h = 2L/N
  *
+ *   dvm_oracle_collide_w takes general decoupled weights instead (eq:decoup,
+ *   B̃(|k|,|l|) w_{k,l} = a(k) b(l)): caller-given a(k) and
+ *   b(l) tabulated over the box [-Ñ,Ñ]^d, and Γ̃_{k,l} = a(k) b(l) on the same
+ *   truncated pair set.
+ *
  *   - "−Ñ ≤ k,l ≤ Ñ" is read componentwise (multi-index convention,
  *     PAPER.md:372-373): DESIGN.md reading R8.
  *   - A nonzero k lies on exactly one line e Z through 0, e = ±k/gcd(k); the
@@ -149,10 +154,20 @@ static int orc_k_allowed(int d, const int *k, int Nbar, int ndirs, const int *di
     return 0;
 }
 
+/* Index of an offset v in [-Ñ,Ñ]^d in a box table (row-major, last axis fastest). */
+static int64_t orc_box_index(int d, int Ntilde, const int *v)
+{
+    int64_t idx = 0;
+    for (int j = 0; j < d; ++j) idx = idx * (2 * Ntilde + 1) + (v[j] + Ntilde);
+    return idx;
+}
+
 /* Step 1: the pair list.  Returns the number of pairs; fills k[], l[] (npairs*d)
- * and a[] when they are non-NULL and cap is large enough. */
-int64_t dvm_oracle_pairs(int d, int Ntilde, int Nbar, double h, int ndirs, const int *dirs,
-                         int64_t cap, int *kout, int *lout, double *aout)
+ * and the pair weights w[] when they are non-NULL and cap is large enough.
+ * wa/wb NULL: Γ̃_{k,l} = a(k) = h^{d+1}|k|/gcd(k) (b = 1); otherwise
+ * Γ̃_{k,l} = wa[k] * wb[l] (eq:decoup), box tables over [-Ñ,Ñ]^d. */
+static int64_t orc_pairs(int d, int Ntilde, int Nbar, double h, int ndirs, const int *dirs, const double *wa,
+                         const double *wb, int64_t cap, int *kout, int *lout, double *aout)
 {
     if (d < 1 || d > ORC_MAXD || Ntilde < 0) return -1;
     int side = 2 * Ntilde + 1;
@@ -172,6 +187,7 @@ int64_t dvm_oracle_pairs(int d, int Ntilde, int Nbar, double h, int ndirs, const
         double norm = 0.0;
         for (int j = 0; j < d; ++j) norm += (double)k[j] * (double)k[j];
         double a = hd1 * sqrt(norm) / (double)g; /* a(k) = h^{d+1}|k|/gcd(k) */
+        if (wa) a = wa[orc_box_index(d, Ntilde, k)];
         for (int64_t cl = 0; cl < box; ++cl) {
             int64_t s = cl;
             for (int j = d - 1; j >= 0; --j) {
@@ -186,12 +202,18 @@ int64_t dvm_oracle_pairs(int d, int Ntilde, int Nbar, double h, int ndirs, const
                     kout[n * d + j] = k[j];
                     lout[n * d + j] = l[j];
                 }
-                aout[n] = a;
+                aout[n] = wb ? a * wb[orc_box_index(d, Ntilde, l)] : a;
             }
             ++n;
         }
     }
     return n;
+}
+
+int64_t dvm_oracle_pairs(int d, int Ntilde, int Nbar, double h, int ndirs, const int *dirs,
+                         int64_t cap, int *kout, int *lout, double *aout)
+{
+    return orc_pairs(d, Ntilde, Nbar, h, ndirs, dirs, NULL, NULL, cap, kout, lout, aout);
 }
 
 static inline void neu_add(double *s, double *c, double x)
@@ -219,15 +241,17 @@ static inline int64_t orc_wrap_index(int d, int N, const int *x, const int *o)
  * (npts < 0: all N^d nodes in storage order; otherwise pts[] holds node
  * indices).  Outputs are [ncells][npts]; any of Q, G, Lo may be NULL.
  * h = 2L/N (reading R3).  ndirs < 0: all lines of order <= N̄; otherwise only
- * the given canonical lines.  Returns 0 on success, negative on bad input. */
-int dvm_oracle_collide(int d, int N, int Nbar, int Ntilde, double L, const double *f,
-                       int64_t ncells, int64_t npts, const int64_t *pts, int ndirs,
-                       const int *dirs, double *Q, double *G, double *Lo, int nthreads)
+ * the given canonical lines.  wa/wb: optional box tables of a(k), b(l)
+ * (see orc_pairs).  Returns 0 on success, negative on bad input. */
+int dvm_oracle_collide_w(int d, int N, int Nbar, int Ntilde, double L, const double *f,
+                         int64_t ncells, int64_t npts, const int64_t *pts, int ndirs,
+                         const int *dirs, const double *wa, const double *wb, double *Q, double *G,
+                         double *Lo, int nthreads)
 {
     if (d < 1 || d > ORC_MAXD || N < 1 || Ntilde < 0 || ncells < 0 || !f) return -1;
     if (npts >= 0 && npts > 0 && !pts) return -1;
     double h = 2.0 * L / (double)N;
-    int64_t cap = dvm_oracle_pairs(d, Ntilde, Nbar, h, ndirs, dirs, 0, NULL, NULL, NULL);
+    int64_t cap = orc_pairs(d, Ntilde, Nbar, h, ndirs, dirs, wa, wb, 0, NULL, NULL, NULL);
     if (cap < 0) return -2;
     int *k = (int *)malloc(sizeof(int) * (size_t)(cap * d + 1));
     int *l = (int *)malloc(sizeof(int) * (size_t)(cap * d + 1));
@@ -237,7 +261,7 @@ int dvm_oracle_collide(int d, int N, int Nbar, int Ntilde, double L, const doubl
         free(k); free(l); free(kl); free(a);
         return -3;
     }
-    dvm_oracle_pairs(d, Ntilde, Nbar, h, ndirs, dirs, cap, k, l, a);
+    orc_pairs(d, Ntilde, Nbar, h, ndirs, dirs, wa, wb, cap, k, l, a);
     for (int64_t p = 0; p < cap * d; ++p) kl[p] = k[p] + l[p];
 
     int64_t nodes = 1;
@@ -281,4 +305,12 @@ int dvm_oracle_collide(int d, int N, int Nbar, int Ntilde, double L, const doubl
     free(kl);
     free(a);
     return 0;
+}
+
+int dvm_oracle_collide(int d, int N, int Nbar, int Ntilde, double L, const double *f,
+                       int64_t ncells, int64_t npts, const int64_t *pts, int ndirs,
+                       const int *dirs, double *Q, double *G, double *Lo, int nthreads)
+{
+    return dvm_oracle_collide_w(d, N, Nbar, Ntilde, L, f, ncells, npts, pts, ndirs, dirs, NULL, NULL, Q, G,
+                                Lo, nthreads);
 }

@@ -55,6 +55,13 @@ def lib():
                                              ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                              ctypes.c_void_p, ctypes.c_int]
             L.dvm_oracle_collide.restype = ctypes.c_int
+            L.dvm_oracle_collide_w.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                               ctypes.c_double, ctypes.c_void_p, ctypes.c_int64,
+                                               ctypes.c_int64, ctypes.c_void_p, ctypes.c_int,
+                                               ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                               ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                               ctypes.c_int]
+            L.dvm_oracle_collide_w.restype = ctypes.c_int
             _lib = L
     return _lib
 
@@ -93,11 +100,15 @@ def _dirs_arg(dirs, d):
 
 def collide(f: np.ndarray, d: int, N: int, Nbar: int, Ntilde: int, L: float = 8.0,
             points: np.ndarray | None = None, dirs: np.ndarray | None = None,
-            nthreads: int = 0):
+            nthreads: int = 0, a_box: np.ndarray | None = None, b_box: np.ndarray | None = None):
     """Direct-sum Q, G, Lo for f of shape [cells, N^d] (or [N]*d / [cells]+[N]*d).
 
     points: optional node indices (row-major) -> outputs [cells, npts];
-    dirs: optional subset of canonical lines (direction-sharding tests).
+    dirs: optional subset of canonical lines (direction-sharding tests);
+    a_box, b_box: optional general decoupled weights a(k), b(l) (eq:decoup,
+    PAPER.md:575-579) tabulated over [-Ñ,Ñ]^d (shape [2Ñ+1]*d, index k + Ñ);
+    Γ̃_{k,l} = a(k) b(l) replaces h^{d+1}|k|/gcd(k) (a_box None: that default;
+    b_box None: b = 1).
     Returns (Q, G, Lo) as float64 arrays of shape [cells, npts or N^d].
     """
     nodes = N ** d
@@ -118,9 +129,17 @@ def collide(f: np.ndarray, d: int, N: int, Nbar: int, Ntilde: int, L: float = 8.
     else:
         keep = np.ascontiguousarray(np.asarray(dirs, dtype=np.int32).reshape(-1, d))
         nd, dp = keep.shape[0], keep.ctypes.data
-    rc = lib().dvm_oracle_collide(d, N, Nbar, Ntilde, float(L), fa.ctypes.data, ncells, npts, pp,
-                                  nd, dp, Q.ctypes.data, G.ctypes.data, Lo.ctypes.data, int(nthreads))
+    box = (2 * Ntilde + 1) ** d
+    wa = None if a_box is None else np.ascontiguousarray(np.asarray(a_box, dtype=np.float64).reshape(-1))
+    wb = None if b_box is None else np.ascontiguousarray(np.asarray(b_box, dtype=np.float64).reshape(-1))
+    for w in (wa, wb):
+        if w is not None and w.size != box:
+            raise ValueError(f"weight tables must have (2Ñ+1)^d = {box} entries")
+    rc = lib().dvm_oracle_collide_w(d, N, Nbar, Ntilde, float(L), fa.ctypes.data, ncells, npts, pp,
+                                    nd, dp, None if wa is None else wa.ctypes.data,
+                                    None if wb is None else wb.ctypes.data, Q.ctypes.data, G.ctypes.data,
+                                    Lo.ctypes.data, int(nthreads))
     if rc != 0:
         raise ValueError(f"dvm_oracle_collide failed with {rc}")
-    del keep, pk
+    del keep, pk, wa, wb
     return Q, G, Lo

@@ -20,6 +20,13 @@ P12 the pseudo-spectral route (eq:sysDiff, eq:betaKL): the
 P13 the box-truncated D^tr (oracle/cross.py) conserves mass,
     momentum and energy for any f, and equals the periodized operator when no
     collision of supp f leaves the box
+P14 general decoupled weights Γ̃_{k,l} = a(k) b(l) (eq:decoup, PAPER.md:575-579;
+    SURVEY §8(f) row 2): the weighted oracle equals the weighted brute force and
+    the weighted dense-β route; mass is conserved for even a and any b, and
+    broken by an odd a; f = const gives 0; a cosine mode cos(2πK.i/N) gives the
+    spatially constant Q = Σ_{(k,l)} a(k) b(l) sin(2πK.k/N) sin(2πK.l/N)
+    (the e_{±2K} terms of the bracket cancel; non-zero only when neither a nor b is even); the default tables reproduce the
+    built-in weights bit for bit
 """
 import itertools
 import math
@@ -408,3 +415,75 @@ def test_p13_truncated_operator_conserves_and_matches_interior(d, N, Nb, Nt):
     Qg = oracle.collide(g.reshape(-1), d, N, Nb, Nt, L)[0].reshape(-1)
     Dg = cross.D_tr(g.reshape(-1), d, N, Nb, Nt, L)
     assert np.abs(Dg - Qg).max() <= 1e-13 * np.abs(Qg).max()
+
+
+# ---------------------------------------------------------------- P14: general weights a(k) b(l)
+def _even_table(d, Nt, seed, lo=0.5, hi=1.5):
+    r = np.random.default_rng(seed).uniform(lo, hi, size=(2 * Nt + 1,) * d)
+    return 0.5 * (r + np.flip(r))  # w(-k) = w(k)
+
+
+@pytest.mark.parametrize("d,N,Nb,Nt", [(2, 8, 2, 3), (2, 10, 3, 4), (3, 6, 1, 2), (3, 7, 2, 3)])
+def test_p14_weighted_oracle_vs_brute_and_dense_beta(d, N, Nb, Nt):
+    from oracle import cross
+    a = _even_table(d, Nt, 100 + N)
+    b = _even_table(d, Nt, 200 + N)
+    L = 4.0
+    f = np.random.default_rng(N + d).uniform(0.0, 1.0, size=(N,) * d)
+    Qo = oracle.collide(f, d, N, Nb, Nt, L, a_box=a, b_box=b)[0].reshape(f.shape)
+    Qb = brute.collide(f, Nb, Nt, 2 * L / N, a_box=a, b_box=b)
+    scale = np.abs(Qb).max()
+    np.testing.assert_allclose(Qo, Qb, rtol=0, atol=1e-13 * scale)
+    Qs, imag = cross.dense_beta_Q(f.reshape(-1), d, N, Nb, Nt, L, a_box=a, b_box=b)
+    assert np.abs(Qs - Qo.reshape(-1)).max() <= 1e-13 * scale and imag <= 1e-13 * scale
+    # the weights enter: the unweighted operator differs
+    assert np.abs(oracle.collide(f, d, N, Nb, Nt, L)[0].reshape(f.shape) - Qo).max() > 1e-3 * scale
+
+
+@pytest.mark.parametrize("d,N,Nb,Nt", [(2, 16, 3, 5), (3, 8, 2, 3)])
+def test_p14_weighted_mass_and_constant(d, N, Nb, Nt):
+    a = _even_table(d, Nt, 7)
+    b = np.random.default_rng(8).uniform(0.0, 2.0, size=(2 * Nt + 1,) * d)  # b need not be even
+    f = np.random.default_rng(9).uniform(0.0, 1.0, N ** d)
+    Q, G, _ = oracle.collide(f, d, N, Nb, Nt, 8.0, a_box=a, b_box=b)
+    assert abs(Q.sum()) <= 1e-13 * G.sum()
+    # an odd part in a breaks the k -> -k pairing that conserves mass
+    a_odd = a * (1.0 + 0.5 * np.sign(np.arange(a.size).reshape(a.shape) - a.size // 2))
+    Q2, G2, _ = oracle.collide(f, d, N, Nb, Nt, 8.0, a_box=a_odd, b_box=b)
+    assert abs(Q2.sum()) > 1e-6 * G2.sum()
+    Qc, Gc, _ = oracle.collide(np.full(N ** d, 0.7), d, N, Nb, Nt, 8.0, a_box=a, b_box=b)
+    assert np.all(Qc == 0.0) and Gc.min() > 0
+
+
+@pytest.mark.parametrize("d,N,Nb,Nt,K", [(2, 16, 3, 5, (1, 2)), (2, 12, 2, 4, (3, 0)), (3, 8, 2, 3, (1, 0, 2))])
+def test_p14_cosine_mode_closed_form(d, N, Nb, Nt, K):
+    from oracle import cross
+    # neither table even: for even a (b) the k -> -k (l -> -l) pairing makes the sum vanish
+    a = np.random.default_rng(30 + d).uniform(0.5, 1.5, size=(2 * Nt + 1,) * d)
+    b = np.random.default_rng(40 + d).uniform(0.5, 1.5, size=(2 * Nt + 1,) * d)
+    grid = np.stack(np.meshgrid(*([np.arange(N)] * d), indexing="ij"), axis=-1).reshape(-1, d)
+    th = 2 * np.pi * np.asarray(K, dtype=np.float64) / N
+    f = np.cos(grid @ th)
+    Q = oracle.collide(f, d, N, Nb, Nt, 8.0, a_box=a, b_box=b)[0].reshape(-1)
+    k, l, _ = cross._pairs(d, N, Nb, Nt, 8.0)
+    w = np.array([a[tuple(kk + Nt)] * b[tuple(ll + Nt)] for kk, ll in zip(k, l)])
+    want = float((w * np.sin(k @ th) * np.sin(l @ th)).sum())
+    assert abs(want) > 1e-3
+    np.testing.assert_allclose(Q, want, rtol=0, atol=1e-12 * np.abs(w).sum())
+
+
+@pytest.mark.parametrize("d,N,Nb,Nt", [(2, 16, 4, 4), (3, 8, 2, 3)])
+def test_p14_default_tables_reproduce_builtin(d, N, Nb, Nt):
+    L = 8.0
+    h = 2 * L / N
+    a = np.zeros((2 * Nt + 1,) * d)
+    for k in itertools.product(range(-Nt, Nt + 1), repeat=d):
+        if any(k):
+            g = 0
+            for c in k:
+                g = math.gcd(g, abs(c))
+            a[tuple(c + Nt for c in k)] = h ** (d + 1) * math.sqrt(sum(c * c for c in k)) / g
+    f = np.random.default_rng(4).uniform(0.0, 1.0, N ** d)
+    Q0 = oracle.collide(f, d, N, Nb, Nt, L)[0]
+    Q1 = oracle.collide(f, d, N, Nb, Nt, L, a_box=a, b_box=np.ones_like(a))[0]
+    assert np.array_equal(Q0, Q1)
