@@ -132,3 +132,10 @@ def random_field(d: int, N: int, seed: int, positive: bool = True) -> np.ndarray
     rng = np.random.default_rng(seed)
     lo = 0.0 if positive else -1.0
     return rng.uniform(lo, 1.0, size=(N,) * d)
+
+
+def even_weights(d: int, Ntilde: int, seed: int, lo: float = 0.5, hi: float = 1.5) -> np.ndarray:
+    """Seeded box table over [-Ñ,Ñ]^d (shape [2Ñ+1]*d, index k + Ñ) with
+    w(-k) = w(k): synthetic decoupled weights a(k) or b(l) (eq:decoup)."""
+    r = np.random.default_rng(seed).uniform(lo, hi, size=(2 * Ntilde + 1,) * d)
+    return 0.5 * (r + np.flip(r))

@@ -196,6 +196,23 @@ DVM_API const char *dvm_profile_name(int k);
  * identical call is bitwise reproducible). */
 DVM_API dvm_status_t dvm_set_path(dvm_plan_t plan, int path);
 
+/* General decoupled collision weights (eq:decoup):
+ * Γ̃_{k,l} = B̃(|k|,|l|) w_{k,l} = a(k) b(l) on the same truncated pair set
+ * (k on the lines of order <= N̄, l ∈ e^⊥ ∩ [-Ñ,Ñ]^d), replacing the built-in
+ * a(k) = h^{d+1}|k|/gcd(k), b = 1 of PAPER.md:582-587.
+ *   a_box, b_box: HOST arrays of (2Ñ+1)^d doubles, row-major over
+ *     [-Ñ,Ñ]^d with index k + Ñ per axis (last axis fastest); copied, the
+ *     caller keeps ownership.  NULL for one table keeps its built-in values;
+ *     both NULL restores the built-in operator (and the fast paths).
+ *   Requirements: finite and even (a(-k) = a(k), b(-l) = b(l): then both
+ *     filter spectra and the loss-kernel spectrum are real); a(0) is unused.
+ *   Evaluation: the spectral path (dvm_set_path 0 or 3; 1 and 2 then return
+ *     DVM_E_STATE at collide time), N in [16, 256], filter tables
+ *     16 A_local N^d bytes <= 4 GB, built on the first collide.
+ *   Errors: DVM_E_NULL (plan), DVM_E_UNSUPPORTED (odd / non-finite weights,
+ *     N out of range; the plan keeps the built-in weights), DVM_E_NOMEM. */
+DVM_API dvm_status_t dvm_set_weights(dvm_plan_t plan, const double *a_box, const double *b_box);
+
 /* Wait for all work issued on the plan's stream; reports asynchronous faults. */
 DVM_API dvm_status_t dvm_sync(dvm_plan_t plan);
 

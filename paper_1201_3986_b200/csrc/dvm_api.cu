@@ -548,6 +548,15 @@ dvm_status_t dvm_set_path(dvm_plan_t P, int path)
     return DVM_OK;
 }
 
+dvm_status_t dvm_set_weights(dvm_plan_t P, const double *a_box, const double *b_box)
+{
+    if (!P) {
+        set_error("NULL argument");
+        return DVM_E_NULL;
+    }
+    return set_weights(P, a_box, b_box);
+}
+
 dvm_status_t dvm_sync(dvm_plan_t P)
 {
     if (!P) {

@@ -353,6 +353,13 @@ dvm_status_t collide_batched(dvm_plan_s *P, const double *f, double *Q, int64_t 
     if (ncells == 0) return DVM_OK;
     // auto: the 3D frame-plane kernel when built; the 2D pair kernels from
     // N = 128 (below, the v1 sweeps are faster: fewer, latency-bound launches)
+    if (P->wt.on) {  // caller weights a(k) b(l): the spectral path evaluates them
+        if (P->path_mode == 1 || P->path_mode == 2) {
+            set_error("custom weights (dvm_set_weights) are evaluated by the spectral path: dvm_set_path 0 or 3");
+            return DVM_E_STATE;
+        }
+        return collide_spectral(P, f, stride, Q, stride, ncells);
+    }
     if (P->path_mode == 3) return collide_spectral(P, f, stride, Q, stride, ncells);
     const bool use_new = P->path_mode == 2 || (P->path_mode == 0 && (P->d == 3 || P->N >= 128));
     if (use_new) {

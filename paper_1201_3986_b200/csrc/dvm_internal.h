@@ -110,6 +110,18 @@ struct GainTables {
     double *that = nullptr;   // spectral path: [A_local][N^d] perp-filter spectra (real)
     size_t bytes = 0;
 };
+
+// Caller weights of the decoupled kernel Γ̃_{k,l} = a(k) b(l) (eq:decoup,
+// PAPER.md:575-579), evaluated by the spectral path only (dvm_set_weights).
+struct WeightTables {
+    bool on = false;
+    double *a_box = nullptr;  // [(2Ñ+1)^d] a(k), index k + Ñ (row-major)
+    double *b_box = nullptr;  // [(2Ñ+1)^d] b(l)
+    double2 *tw = nullptr;    // FFT twiddles
+    double *lamhat = nullptr; // [N^d] spectrum of the weighted loss kernel λ_w (real)
+    double *shat = nullptr;   // [A_local][N^d] weighted line-filter spectra (lazy)
+    double *that = nullptr;   // [A_local][N^d] weighted perp-filter spectra (lazy)
+};
 }  // namespace dvm
 
 struct dvm_plan_s {
@@ -127,6 +139,7 @@ struct dvm_plan_s {
     std::vector<uint8_t> is_local;
     dvm::Workspace ws;
     dvm::GainTables g;
+    dvm::WeightTables wt;
     uint64_t launches = 0;
     size_t table_bytes = 0;
     bool profiling = false;
@@ -214,6 +227,8 @@ dvm_status_t reduce_slots(dvm_plan_s *P, double *Q, int64_t q_stride, const doub
                           int nslots, int64_t ncells, int64_t nodes);
 // 3D gain (dvm_gain3d.cu), loss as one FFT convolution (dvm_loss.cu)
 dvm_status_t build_loss(dvm_plan_s *P);
+dvm_status_t set_weights(dvm_plan_s *P, const double *a_box, const double *b_box);
+void free_weights(dvm_plan_s *P);
 dvm_status_t loss_init(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q, int64_t q_stride, int64_t ncells,
                        double2 *QI);
 dvm_status_t collide_spectral(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q, int64_t q_stride,

@@ -16,6 +16,8 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <cmath>
+#include <vector>
 
 #include "dvm_internal.h"
 
@@ -181,6 +183,49 @@ __global__ void k_lambda(int d, int N, int p, int Nt, const int *local, int nloc
     lam[j] = acc;
 }
 
+// Weighted loss kernel (eq:decoup, general a(k) b(l)):
+//   λ_w(j) = Σ_e Σ_{1<=|m|<=M_e, l ∈ e^⊥ ∩ [-Ñ,Ñ]^d, me + l ≡ j} a(me) b(l)
+// (2Ñ+1 <= N: at most one l per residue class).  Box tables indexed k + Ñ.
+__device__ __forceinline__ int box_index(int d, int Nt, const int *v)
+{
+    int idx = 0;
+    for (int q = 0; q < d; ++q) idx = idx * (2 * Nt + 1) + (v[q] + Nt);
+    return idx;
+}
+
+__global__ void k_lambda_w(int d, int N, int p, int Nt, const int *local, int nloc, const int *E, const int *M,
+                           const double *wa, const double *wb, double *lam)
+{
+    int64_t nodes = 1;
+    for (int q = 0; q < d; ++q) nodes *= N;
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= nodes) return;
+    int jc[3] = {0, 0, 0};
+    for (int q = d - 1, sh = 0; q >= 0; --q, sh += p) jc[q] = (int)((j >> sh) & (N - 1));
+    double acc = 0.0;
+    for (int k = 0; k < nloc; ++k) {
+        const int di = local[k];
+        const int ee[3] = {E[3 * di], E[3 * di + 1], E[3 * di + 2]};
+        const int m_e = M[di];
+        for (int m = 1; m <= m_e; ++m)
+            for (int s = -1; s <= 1; s += 2) {
+                bool ok = true;
+                int dot = 0, kv[3] = {0, 0, 0}, lv[3] = {0, 0, 0};
+                for (int q = 0; q < d; ++q) {
+                    kv[q] = s * m * ee[q];
+                    int v = (jc[q] - kv[q]) % N;
+                    if (v < 0) v += N;
+                    if (v > N / 2) v -= N;
+                    if (v > Nt || v < -Nt) ok = false;
+                    lv[q] = v;
+                    dot += v * ee[q];
+                }
+                if (ok && dot == 0) acc += wa[box_index(d, Nt, kv)] * wb[box_index(d, Nt, lv)];
+            }
+    }
+    lam[j] = acc;
+}
+
 __global__ void k_take_real(const double2 *z, int64_t n, double *out)
 {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -258,6 +303,63 @@ __global__ void k_spec_tables(int d, int N, int p, int nloc, const int *local, c
     that[(int64_t)k * nodes + j] = th;
 }
 
+// Weighted filters (even a, b): ŝ_e(ξ) = Σ_{m=1}^{M_e} 2 a(me) cos(2π m e.ξ/N),
+// t̂_e(ξ) = Σ_{l ∈ P_e} b(l) cos(2π l.ξ/N); a(me) sits in ŝ_e (Q += S_e T_e).
+__global__ void k_spec_tables_w(int d, int N, int p, int Nt, int nloc, const int *local, const int *E, const int *M,
+                                const int *U, const int *W, const int *row_off, const int *row_b,
+                                const int *row_lo, const int *row_hi, const double *ctab, const double *wa,
+                                const double *wb, double *shat, double *that)
+{
+    int64_t nodes = 1;
+    for (int q = 0; q < d; ++q) nodes *= N;
+    const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= nodes * nloc) return;
+    const int k = (int)(gid / nodes);
+    const int64_t j = gid % nodes;
+    int xi[3] = {0, 0, 0};
+    for (int q = d - 1, sh = 0; q >= 0; --q, sh += p) xi[q] = (int)((j >> sh) & (N - 1));
+    const int di = local[k];
+    const int *e = E + 3 * di;
+    int ev = 0;
+    for (int q = 0; q < d; ++q) ev += e[q] * xi[q];
+    ev %= N;
+    if (ev < 0) ev += N;
+    const int m_e = M[di];
+    double sh_ = 0.0;
+    for (int m = 1; m <= m_e; ++m) {
+        const int kv[3] = {m * e[0], m * e[1], m * e[2]};
+        sh_ += 2.0 * wa[box_index(d, Nt, kv)] * ctab[(m * ev) & (N - 1)];
+    }
+    double th = 0.0;
+    if (d == 2) {
+        const int ep[2] = {-e[1], e[0]};
+        int pv = (ep[0] * xi[0] + ep[1] * xi[1]) % N;
+        if (pv < 0) pv += N;
+        for (int n = -m_e; n <= m_e; ++n) {
+            const int lv[3] = {n * ep[0], n * ep[1], 0};
+            th += wb[box_index(2, Nt, lv)] * ctab[((n * pv) % N + N) & (N - 1)];
+        }
+    } else {
+        const int *u = U + 3 * di, *w = W + 3 * di;
+        int uv = 0, wv = 0;
+        for (int q = 0; q < 3; ++q) {
+            uv += u[q] * xi[q];
+            wv += w[q] * xi[q];
+        }
+        uv = ((uv % N) + N) % N;
+        wv = ((wv % N) + N) % N;
+        for (int r = row_off[di]; r < row_off[di + 1]; ++r) {
+            const int b = row_b[r];
+            for (int a = row_lo[r]; a <= row_hi[r]; ++a) {
+                const int lv[3] = {a * u[0] + b * w[0], a * u[1] + b * w[1], a * u[2] + b * w[2]};
+                th += wb[box_index(3, Nt, lv)] * ctab[(((a * uv + b * wv) % N) + N) & (N - 1)];
+            }
+        }
+    }
+    shat[(int64_t)k * nodes + j] = sh_;
+    that[(int64_t)k * nodes + j] = th;
+}
+
 __global__ void k_cos_table(int N, double *ctab)
 {
     const int n = blockIdx.x * blockDim.x + threadIdx.x;
@@ -287,6 +389,55 @@ __global__ void k_spec_acc(const double2 *__restrict__ z, double aw, double scal
 }  // namespace
 
 
+// λ (computed by `fill` into a scratch array) -> its real spectrum `lamhat`
+// (λ even: FFT(λ) is real), with twiddles `tw`.
+template <typename Fill>
+dvm_status_t lambda_spectrum(dvm_plan_s *P, const double2 *tw, double *lamhat, Fill fill)
+{
+    const int d = P->d, N = P->N;
+    int64_t nodes = 1;
+    for (int j = 0; j < d; ++j) nodes *= N;
+    double *lam = nullptr;
+    double2 *z = nullptr;
+    DVM_CUDA(cudaMalloc(&lam, sizeof(double) * nodes));
+    if (cudaMalloc(&z, sizeof(double2) * nodes) != cudaSuccess) {
+        cudaFree(lam);
+        return cuda_fail(cudaGetLastError(), "cudaMalloc");
+    }
+    {
+        LaunchScope ls(P, KC_PLAN);
+        fill(lam, nodes);
+    }
+    const cudaError_t le = cudaGetLastError();
+    dvm_status_t st = le == cudaSuccess ? DVM_OK : cuda_fail(le, "k_lambda");
+    for (int k = 0; k < d && !st; ++k) {
+        FftArgs a = {};
+        a.d = d;
+        a.npairs = 1;
+        a.tw = tw;
+        a.r_cells = 1;
+        a.r_first = 0;
+        a.ax = d - 1 - k;
+        a.zin = z;
+        a.zout = z;
+        if (k == 0) {
+            a.r0 = lam;
+            a.r_stride = nodes;
+        }
+        st = fft_dispatch(P, a);
+    }
+    if (!st) {
+        LaunchScope ls(P, KC_PLAN);
+        k_take_real<<<256, 256, 0, P->stream>>>(z, nodes, lamhat);
+    }
+    cudaStreamSynchronize(P->stream);
+    cudaFree(lam);
+    cudaFree(z);
+    if (st) return st;
+    DVM_CUDA(cudaGetLastError());
+    return DVM_OK;
+}
+
 // Plan-time tables of the loss: twiddles, λ of the plan's (local) directions
 // and its real spectrum λ̂.
 dvm_status_t build_loss(dvm_plan_s *P)
@@ -302,43 +453,100 @@ dvm_status_t build_loss(dvm_plan_s *P)
         LaunchScope ls(P, KC_PLAN);
         k_twiddles<<<1, 128, 0, P->stream>>>(N, g.tw);
     }
-    double *lam = nullptr;
-    double2 *z = nullptr;
-    DVM_CUDA(cudaMalloc(&lam, sizeof(double) * nodes));
-    DVM_CUDA(cudaMalloc(&z, sizeof(double2) * nodes));
+    return lambda_spectrum(P, g.tw, g.lamhat, [&](double *lam, int64_t n) {
+        k_lambda<<<(unsigned)((n + 127) / 128), 128, 0, P->stream>>>(d, N, P->p, P->Ntilde, P->t.local,
+                                                                     (int)P->local.size(), P->t.e, P->t.M, P->t.a,
+                                                                     lam);
+    });
+}
+
+void free_weights(dvm_plan_s *P)
+{
+    WeightTables &w = P->wt;
+    if (w.a_box || w.tw) cudaStreamSynchronize(P->stream);
+    void *ptrs[] = {w.a_box, w.b_box, w.tw, w.lamhat, w.shat, w.that};
+    for (void *q : ptrs)
+        if (q) cudaFree(q);
+    w = WeightTables{};
+}
+
+// dvm_set_weights: validate the box tables (finite, even), upload them and
+// build the weighted loss spectrum; the filter spectra follow lazily.
+dvm_status_t set_weights(dvm_plan_s *P, const double *a_box, const double *b_box)
+{
+    free_weights(P);
+    if (!a_box && !b_box) return DVM_OK;  // back to the built-in weights
+    const int d = P->d, N = P->N, Nt = P->Ntilde;
+    if (N < 16 || N > 256) {
+        set_error("custom weights need the spectral path: N in [16, 256]");
+        return DVM_E_UNSUPPORTED;
+    }
+    const int side = 2 * Nt + 1;
+    int64_t box = 1;
+    for (int j = 0; j < d; ++j) box *= side;
+    std::vector<double> a(box), b(box);
+    for (int64_t i = 0; i < box; ++i) {
+        int v[3] = {0, 0, 0};
+        int64_t r = i;
+        for (int j = d - 1; j >= 0; --j) {
+            v[j] = (int)(r % side) - Nt;
+            r /= side;
+        }
+        if (a_box) {
+            a[i] = a_box[i];
+        } else {  // built-in a(k) = h^{d+1} |k| / gcd(k)
+            int g = 0;
+            double n2 = 0.0;
+            for (int j = 0; j < d; ++j) {
+                int x = v[j] < 0 ? -v[j] : v[j], y = g;
+                while (y) {
+                    const int t = x % y;
+                    x = y;
+                    y = t;
+                }
+                g = x;
+                n2 += (double)v[j] * v[j];
+            }
+            a[i] = g ? pow(P->h, d + 1) * sqrt(n2) / g : 0.0;
+        }
+        b[i] = b_box ? b_box[i] : 1.0;
+    }
+    for (int64_t i = 0; i < box; ++i) {
+        // reversing the row-major index negates every coordinate
+        if (!std::isfinite(a[i]) || !std::isfinite(b[i]) || a[i] != a[box - 1 - i] || b[i] != b[box - 1 - i]) {
+            set_error("weights must be finite and even: a(-k) = a(k), b(-l) = b(l)");
+            return DVM_E_UNSUPPORTED;
+        }
+    }
+    WeightTables &w = P->wt;
+    int64_t nodes = 1;
+    for (int j = 0; j < d; ++j) nodes *= N;
+    if (cudaMalloc(&w.a_box, sizeof(double) * box) != cudaSuccess ||
+        cudaMalloc(&w.b_box, sizeof(double) * box) != cudaSuccess ||
+        cudaMalloc(&w.tw, sizeof(double2) * N / 2) != cudaSuccess ||
+        cudaMalloc(&w.lamhat, sizeof(double) * nodes) != cudaSuccess) {
+        cudaGetLastError();
+        free_weights(P);
+        set_error("weight table allocation failed");
+        return DVM_E_NOMEM;
+    }
+    DVM_CUDA(cudaMemcpyAsync(w.a_box, a.data(), sizeof(double) * box, cudaMemcpyHostToDevice, P->stream));
+    DVM_CUDA(cudaMemcpyAsync(w.b_box, b.data(), sizeof(double) * box, cudaMemcpyHostToDevice, P->stream));
     {
         LaunchScope ls(P, KC_PLAN);
-        k_lambda<<<(unsigned)((nodes + 127) / 128), 128, 0, P->stream>>>(d, N, P->p, P->Ntilde, P->t.local,
-                                                                         (int)P->local.size(), P->t.e, P->t.M,
-                                                                         P->t.a, lam);
+        k_twiddles<<<1, 128, 0, P->stream>>>(N, w.tw);
     }
-    const cudaError_t le = cudaGetLastError();
-    dvm_status_t st = le == cudaSuccess ? DVM_OK : cuda_fail(le, "k_lambda");
-    for (int k = 0; k < d && !st; ++k) {
-        FftArgs a = {};
-        a.d = d;
-        a.npairs = 1;
-        a.tw = g.tw;
-        a.r_cells = 1;
-        a.r_first = 0;
-        a.ax = d - 1 - k;
-        a.zin = z;
-        a.zout = z;
-        if (k == 0) {
-            a.r0 = lam;
-            a.r_stride = nodes;
-        }
-        st = fft_dispatch(P, a);
+    const double *wa = w.a_box, *wb = w.b_box;
+    dvm_status_t st = lambda_spectrum(P, w.tw, w.lamhat, [&](double *lam, int64_t n) {
+        k_lambda_w<<<(unsigned)((n + 127) / 128), 128, 0, P->stream>>>(d, N, P->p, Nt, P->t.local,
+                                                                       (int)P->local.size(), P->t.e, P->t.M, wa,
+                                                                       wb, lam);
+    });
+    if (st) {
+        free_weights(P);
+        return st;
     }
-    if (!st) {
-        LaunchScope ls(P, KC_PLAN);
-        k_take_real<<<256, 256, 0, P->stream>>>(z, nodes, g.lamhat);
-    }
-    cudaStreamSynchronize(P->stream);
-    cudaFree(lam);
-    cudaFree(z);
-    if (st) return st;
-    DVM_CUDA(cudaGetLastError());
+    w.on = true;
     return DVM_OK;
 }
 
@@ -355,13 +563,15 @@ dvm_status_t loss_init(dvm_plan_s *P, const double *f, int64_t f_stride, double 
     dvm_status_t st;
     if ((st = grow(&w.fft_z, &w.fft_z_elems, (size_t)(batch * nodes), P->stream))) return st;
     double scale = 1.0 / (double)nodes;
+    const double2 *tw = P->wt.on ? P->wt.tw : P->g.tw;
+    const double *lamhat = P->wt.on ? P->wt.lamhat : P->g.lamhat;
     for (int64_t p0 = 0; p0 < npairs_all; p0 += batch) {
         const int64_t np = std::min(batch, npairs_all - p0);
         for (int k = 0; k < 2 * d; ++k) {
             FftArgs a = {};
             a.d = d;
             a.npairs = np;
-            a.tw = P->g.tw;
+            a.tw = tw;
             a.r_cells = ncells;
             a.r_first = 2 * p0;
             const bool fwd = k < d;
@@ -373,7 +583,7 @@ dvm_status_t loss_init(dvm_plan_s *P, const double *f, int64_t f_stride, double 
                 a.r0 = f;
                 a.r_stride = f_stride;
             }
-            if (k == d - 1) a.mult = P->g.lamhat;
+            if (k == d - 1) a.mult = lamhat;
             if (k == 2 * d - 1) {
                 a.qI = QI;
                 a.q = Q;
@@ -397,7 +607,9 @@ dvm_status_t collide_spectral(dvm_plan_s *P, const double *f, int64_t f_stride, 
     for (int j = 0; j < d; ++j) nodes *= N;
     const int nloc = (int)P->local.size();
     GainTables &g = P->g;
-    if (!g.lamhat) {
+    WeightTables &wt = P->wt;
+    const bool wtd = wt.on;  // caller weights a(k) b(l) (dvm_set_weights)
+    if (!wtd && !g.lamhat) {
         set_error("spectral path needs the FFT loss tables (3D N in {32, 64}, 2D 16 <= N <= 256)");
         return DVM_E_UNSUPPORTED;
     }
@@ -407,18 +619,26 @@ dvm_status_t collide_spectral(dvm_plan_s *P, const double *f, int64_t f_stride, 
     }
     dvm_status_t st;
     Workspace &w = P->ws;
-    if (!g.shat && nloc > 0) {  // lazily, on first use
-        DVM_CUDA(cudaMalloc(&g.shat, sizeof(double) * nodes * nloc));
-        DVM_CUDA(cudaMalloc(&g.that, sizeof(double) * nodes * nloc));
+    double *&shat = wtd ? wt.shat : g.shat;
+    double *&that = wtd ? wt.that : g.that;
+    const double2 *tw = wtd ? wt.tw : g.tw;
+    if (!shat && nloc > 0) {  // lazily, on first use
+        DVM_CUDA(cudaMalloc(&shat, sizeof(double) * nodes * nloc));
+        DVM_CUDA(cudaMalloc(&that, sizeof(double) * nodes * nloc));
         double *ctab = nullptr;
         DVM_CUDA(cudaMalloc(&ctab, sizeof(double) * N));
         {
             LaunchScope ls(P, KC_PLAN);
             k_cos_table<<<(N + 127) / 128, 128, 0, P->stream>>>(N, ctab);
             const int64_t tot = nodes * nloc;
-            k_spec_tables<<<(unsigned)((tot + 127) / 128), 128, 0, P->stream>>>(
-                d, N, P->p, nloc, P->t.local, P->t.e, P->t.M, P->t.u, P->t.w, P->t.row_off, P->t.row_b,
-                P->t.row_lo, P->t.row_hi, ctab, g.shat, g.that);
+            if (wtd)
+                k_spec_tables_w<<<(unsigned)((tot + 127) / 128), 128, 0, P->stream>>>(
+                    d, N, P->p, P->Ntilde, nloc, P->t.local, P->t.e, P->t.M, P->t.u, P->t.w, P->t.row_off,
+                    P->t.row_b, P->t.row_lo, P->t.row_hi, ctab, wt.a_box, wt.b_box, shat, that);
+            else
+                k_spec_tables<<<(unsigned)((tot + 127) / 128), 128, 0, P->stream>>>(
+                    d, N, P->p, nloc, P->t.local, P->t.e, P->t.M, P->t.u, P->t.w, P->t.row_off, P->t.row_b,
+                    P->t.row_lo, P->t.row_hi, ctab, shat, that);
         }
         DVM_CUDA(cudaGetLastError());
         DVM_CUDA(cudaStreamSynchronize(P->stream));
@@ -434,7 +654,7 @@ dvm_status_t collide_spectral(dvm_plan_s *P, const double *f, int64_t f_stride, 
             FftArgs a = {};
             a.d = d;
             a.npairs = 1;
-            a.tw = g.tw;
+            a.tw = tw;
             a.r_cells = 1;
             a.ax = d - 1 - k;
             a.zin = z0;
@@ -448,14 +668,14 @@ dvm_status_t collide_spectral(dvm_plan_s *P, const double *f, int64_t f_stride, 
         for (int kd = 0; kd < nloc; ++kd) {
             {
                 LaunchScope ls(P, KC_FFT);
-                k_spec_mul<<<256, 256, 0, P->stream>>>(z0, g.shat + (int64_t)kd * nodes, g.that + (int64_t)kd * nodes,
+                k_spec_mul<<<256, 256, 0, P->stream>>>(z0, shat + (int64_t)kd * nodes, that + (int64_t)kd * nodes,
                                                      z1, nodes);
             }
             for (int k = 0; k < d; ++k) {
                 FftArgs a = {};
                 a.d = d;
                 a.npairs = 1;
-                a.tw = g.tw;
+                a.tw = tw;
                 a.inverse = 1;
                 a.ax = k;
                 a.zin = z1;
@@ -463,8 +683,10 @@ dvm_status_t collide_spectral(dvm_plan_s *P, const double *f, int64_t f_stride, 
                 if ((st = fft_dispatch(P, a))) return st;
             }
             {
+                // weighted: a(me) is inside ŝ_e; built-in: the line constant a_e
+                const double aw = wtd ? 1.0 : P->h_a[P->local[kd]];
                 LaunchScope ls(P, KC_FFT);
-                k_spec_acc<<<256, 256, 0, P->stream>>>(z1, P->h_a[P->local[kd]], scale, Q + c * q_stride, nodes);
+                k_spec_acc<<<256, 256, 0, P->stream>>>(z1, aw, scale, Q + c * q_stride, nodes);
             }
         }
         DVM_CUDA(cudaGetLastError());

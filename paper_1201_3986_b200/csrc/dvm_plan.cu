@@ -463,6 +463,7 @@ void free_table(dvm_plan_s *P)
         if (q) cudaFree(q);
     t = DirTable{};
     free_gain3d(P);
+    free_weights(P);
 }
 
 }  // namespace dvm

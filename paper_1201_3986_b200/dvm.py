@@ -81,6 +81,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "dvm_profile_read": ([P, V, V, ctypes.c_int], ctypes.c_int),
         "dvm_profile_name": ([ctypes.c_int], ctypes.c_char_p),
         "dvm_set_path": ([P, ctypes.c_int], ctypes.c_int),
+        "dvm_set_weights": ([P, V, V], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -249,8 +250,25 @@ class Plan:
         _check(load().dvm_set_graphs(self._h, 1 if enable else 0), "dvm_set_graphs")
 
     def set_path(self, path: int):
-        """0 = default kernels, 1 = v1 orbit sweeps (cross-check path)."""
+        """0 = auto, 1 = v1 orbit sweeps, 2 = FFT-loss kernels, 3 = spectral reference."""
         _check(load().dvm_set_path(self._h, int(path)), "dvm_set_path")
+
+    def set_weights(self, a_box=None, b_box=None):
+        """General decoupled weights a(k), b(l) (eq:decoup) as host arrays of shape
+        [2Ñ+1]*d indexed by k + Ñ (None: built-in values; both None: built-in operator)."""
+        import numpy as np
+        side = 2 * self.Ntilde + 1
+        arrs = []
+        for w in (a_box, b_box):
+            if w is None:
+                arrs.append(None)
+                continue
+            w = np.ascontiguousarray(np.asarray(w, dtype=np.float64))
+            if w.size != side ** self.d:
+                raise ValueError(f"weight tables need (2Ñ+1)^d = {side ** self.d} entries")
+            arrs.append(w)
+        _check(load().dvm_set_weights(self._h, *(None if w is None else w.ctypes.data for w in arrs)),
+               "dvm_set_weights")
 
     def profile(self, enable: bool = True):
         """Start (clear) / stop per-kernel CUDA-event timing inside libdvm."""

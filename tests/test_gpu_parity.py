@@ -442,3 +442,69 @@ def test_triple_agreement_c1():
     for path in (0, 1, 2, 3):
         p.set_path(path)
         _assert_parity(_gpu(p, f).reshape(-1), Qb, f"path {path} vs dense beta")
+
+
+# ---------------------------------------------------------------- general weights a(k) b(l) (dvm_set_weights)
+@pytest.mark.parametrize("d,N,Nbar,Nt,cells", [(2, 16, 4, 4, 1), (2, 64, 8, 14, 3), (3, 16, 2, 3, 2), (3, 32, 2, 5, 1)])
+def test_weighted_spectral_matches_oracle(d, N, Nbar, Nt, cells):
+    """Γ̃_{k,l} = a(k) b(l) with seeded even tables (eq:decoup):
+    the spectral path against the weighted oracle; mass conserved."""
+    a = dvm_inputs.even_weights(d, Nt, 10 + N)
+    b = dvm_inputs.even_weights(d, Nt, 20 + N, 0.2, 1.0)
+    f = np.stack([dvm_inputs.two_bumps(d, N, 8.0, 1.0 + 0.2 * c, 0.01, c).reshape(-1) for c in range(cells)])
+    p = _plan(d, N, Nbar, Ntilde=Nt)
+    p.set_weights(a, b)
+    q = _gpu(p, f)
+    pts = None if N ** d <= 4096 else np.arange(0, N ** d, N ** d // 197)
+    for c in range(cells):
+        Qo, Go, _ = oracle.collide(f[c], d, N, Nbar, Nt, 8.0, points=pts, a_box=a, b_box=b)
+        qc = q[c] if pts is None else q[c][pts]
+        _assert_parity(qc, Qo[0], f"weighted d={d} N={N} cell {c}")
+        assert abs(q[c].sum()) <= 1e-12 * np.abs(q[c]).sum()
+    # the weights enter: the built-in operator differs
+    p.set_weights(None, None)
+    q0 = _gpu(p, f)
+    assert np.abs(q0 - q).max() > 1e-3 * np.abs(q).max()
+
+
+@pytest.mark.parametrize("d,N,Nbar,Nt", [(2, 64, 8, 14), (3, 32, 4, 7)])
+def test_weighted_builtin_tables_equal_default_path(d, N, Nbar, Nt):
+    """The built-in a(k) = h^{d+1}|k|/gcd(k), b = 1 passed as tables reproduces
+    the default path (to rounding): the weighted λ and filters index the box right."""
+    p = _plan(d, N, Nbar, Ntilde=Nt)
+    h = p.h
+    a = np.zeros((2 * Nt + 1,) * d)
+    for k in itertools.product(range(-Nt, Nt + 1), repeat=d):
+        if any(k):
+            g = 0
+            for c in k:
+                g = math.gcd(g, abs(c))
+            a[tuple(c + Nt for c in k)] = h ** (d + 1) * math.sqrt(sum(c * c for c in k)) / g
+    f = np.stack([dvm_inputs.two_bumps(d, N, 8.0, 1.3, 0.01, 5).reshape(-1)] * 2)
+    q0 = _gpu(p, f)
+    p.set_weights(a, np.ones_like(a))
+    q1 = _gpu(p, f)
+    np.testing.assert_allclose(q1, q0, rtol=0, atol=1e-12 * np.abs(q0).max())
+    p.set_weights(a, None)  # None keeps b = 1
+    np.testing.assert_allclose(_gpu(p, f), q0, rtol=0, atol=1e-12 * np.abs(q0).max())
+
+
+def test_weighted_errors_and_reset():
+    from paper_1201_3986_b200 import DvmError
+    p = _plan(2, 16, 4, Ntilde=4)
+    f = dvm_inputs.make("c1")[0]
+    q_default = _gpu(p, f)
+    odd = np.arange(81, dtype=np.float64).reshape(9, 9)
+    with pytest.raises(DvmError):
+        p.set_weights(odd, None)
+    np.testing.assert_array_equal(_gpu(p, f), q_default)  # rejected tables leave the plan unchanged
+    p.set_weights(dvm_inputs.even_weights(2, 4, 1), None)
+    for path in (1, 2):
+        p.set_path(path)
+        with pytest.raises(DvmError):
+            _gpu(p, f)
+    p.set_path(3)
+    _gpu(p, f)
+    p.set_weights(None, None)
+    p.set_path(0)
+    np.testing.assert_array_equal(_gpu(p, f), q_default)
