@@ -351,17 +351,24 @@ dvm_status_t collide_batched(dvm_plan_s *P, const double *f, double *Q, int64_t 
 {
     const Geo g = geo_of(P);
     if (ncells == 0) return DVM_OK;
-    // auto: the 3D frame-plane kernel when built; the 2D pair kernels from
-    // N = 128 (below, the v1 sweeps are faster: fewer, latency-bound launches)
+    // auto: 3D N = 64 the FFT-filter gain, other 3D the frame-plane kernel when
+    // built; the 2D pair kernels from N = 128 (below, the v1 sweeps are faster:
+    // fewer, latency-bound launches)
     if (P->wt.on) {  // caller weights a(k) b(l): the spectral path evaluates them
-        if (P->path_mode == 1 || P->path_mode == 2) {
+        if (P->path_mode == 1 || P->path_mode == 2 || P->path_mode == 4) {
             set_error("custom weights (dvm_set_weights) are evaluated by the spectral path: dvm_set_path 0 or 3");
             return DVM_E_STATE;
         }
         return collide_spectral(P, f, stride, Q, stride, ncells);
     }
     if (P->path_mode == 3) return collide_spectral(P, f, stride, Q, stride, ncells);
-    const bool use_new = P->path_mode == 2 || (P->path_mode == 0 && (P->d == 3 || P->N >= 128));
+    // auto for 3D N = 64: the FFT-filter gain (faster than the frame-plane kernel)
+    if (P->path_mode == 4 || (P->path_mode == 0 && P->d == 3 && P->N == 64)) {
+        bool handled = false;
+        dvm_status_t st = collide_fgain3d(P, f, stride, Q, stride, ncells, &handled);
+        if (st || handled) return st;
+    }
+    const bool use_new = P->path_mode == 2 || P->path_mode == 4 || (P->path_mode == 0 && (P->d == 3 || P->N >= 128));
     if (use_new) {
         bool handled = false;
         dvm_status_t st = P->d == 3 ? collide_gain3d(P, f, stride, Q, stride, ncells, &handled)
@@ -507,7 +514,7 @@ void free_workspace(dvm_plan_s *P)
 {
     clear_profile(P);
     Workspace &w = P->ws;
-    void *ptrs[] = {w.S, w.part, w.f_stage, w.q_stage, w.mom_partial, w.mom_dev, w.qtmp, w.f1tmp, w.mom_ctr, w.fft_z, w.g3_f, w.g3_t, w.g3_q, w.g3_ctr, w.p2_scr, w.p2_part, w.sp_z};
+    void *ptrs[] = {w.S, w.part, w.f_stage, w.q_stage, w.mom_partial, w.mom_dev, w.qtmp, w.f1tmp, w.mom_ctr, w.fft_z, w.g3_f, w.g3_t, w.g3_q, w.g3_ctr, w.p2_scr, w.p2_part, w.sp_z, w.fg_fhat};
     for (void *q : ptrs)
         if (q) cudaFree(q);
     w = Workspace{};

@@ -29,12 +29,13 @@
 #include <vector>
 
 #include "dvm_frame.h"
+#include "dvm_g3common.h"
 #include "dvm_internal.h"
 
 namespace dvm {
 namespace {
+using namespace g3;
 
-constexpr int kCL = 16;         // CTAs per cell group
 constexpr int kMaxRec = 72;     // int4 words of a direction record (6 meta + program entries)
 constexpr int kMaxMS = 32;      // line half-width M_e held in shared memory
 
@@ -55,77 +56,8 @@ struct GainArgs {
 };
 
 constexpr int kSlots = 2;   // T ring depth per group (phase A may run kSlots-1 steps ahead)
-constexpr int kRoleT = 256; // threads per role (warps 0-7: phase A, warps 8-15: phase B)
 
-template <int N>
-__device__ __forceinline__ uint32_t pk(int c0, int c1, int c2)
-{
-    constexpr int P = N == 32 ? 5 : 6;
-    return ((uint32_t)(c0 & (N - 1)) << (2 * P)) | ((uint32_t)(c1 & (N - 1)) << P) | (uint32_t)(c2 & (N - 1));
-}
 
-__device__ __forceinline__ void role_sync(int id) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kRoleT) : "memory"); }
-
-// Wait until every CTA of the group has published progress >= target on its
-// own monotonic counter (ctrs[0..kCL)): lanes of the role's first warp poll one
-// counter each (acquire), then the role syncs.  Per-CTA counters, not a sum:
-// a CTA running ahead must not stand in for a slower one.
-__device__ __forceinline__ void role_wait(const unsigned int *ctrs, unsigned int target, int t, int id)
-{
-    if (t < 32) {
-        bool ok = t >= kCL;
-        for (;;) {
-            if (!ok) {
-                unsigned int v;
-                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctrs + t) : "memory");
-                ok = v >= target;
-            }
-            if (__all_sync(0xffffffffu, ok)) break;
-            __nanosleep(32);
-        }
-    }
-    role_sync(id);
-}
-
-// publish this CTA's role progress (all of the role's writes so far first)
-__device__ __forceinline__ void role_signal(unsigned int *own, unsigned int value, bool leader, int id)
-{
-    role_sync(id);
-    if (leader) {
-        __threadfence();
-        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(own), "r"(value) : "memory");
-    }
-}
-
-// ---- tensor memory (TMEM) as the phase-B accumulator store: each B-role thread
-// owns one TMEM lane and 256 32-bit columns (its 64 nodes × 2 cells in fp64).
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16])
-{
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-        "%15}, [%16];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16])
-{
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-        "%15, %16};" ::"r"(taddr),
-        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
-        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
-        : "memory");
-}
-__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-
-__device__ __forceinline__ double2 add2(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ double2 sub2(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
-__device__ __forceinline__ double2 fma2(double s, double2 a, double2 c)
-{
-    return make_double2(fma(s, a.x, c.x), fma(s, a.y, c.y));
-}
 
 // Shared-memory geometry (one lattice plane of a cell pair at a time).  Rows
 // are padded to RS = N + 1 double2 (a thread-per-row scan is then bank-conflict
@@ -148,46 +80,6 @@ struct G3Geom {
                                    sizeof(uint32_t) * 2 * kMaxMS;
 };
 
-// L2 residency policies: the T ring and f stay (evict_last); T once consumed
-// and the per-pair Q init/final go first (evict_first).
-__device__ __forceinline__ uint64_t l2_keep()
-{
-    uint64_t p;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-__device__ __forceinline__ uint64_t l2_drop()
-{
-    uint64_t p;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-__device__ __forceinline__ void st2_hint(double2 *a, double2 v, uint64_t pol)
-{
-    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(a), "d"(v.x), "d"(v.y), "l"(pol) : "memory");
-}
-__device__ __forceinline__ double2 ld2_cg_hint(const double2 *a, uint64_t pol)
-{
-    double2 v;
-    asm volatile("ld.global.cg.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(a), "l"(pol));
-    return v;
-}
-__device__ __forceinline__ double2 ld2_nc_hint(const double2 *a, uint64_t pol)
-{
-    double2 v;
-    asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(a), "l"(pol));
-    return v;
-}
-
-__device__ __forceinline__ void cp_async16(void *smem_dst, const void *gsrc)
-{
-    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(
-                     (uint32_t)__cvta_generic_to_shared(smem_dst)),
-                 "l"(gsrc), "l"(l2_keep())
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 // Gather lattice plane g (frame z, u, w) of a cell pair into dst[ROWS][RS]
 // (rows < L also into their duplicate rows) with 16-byte cp.async requests.
@@ -724,10 +616,28 @@ dvm_status_t build_gain3d(dvm_plan_s *P)
 void free_gain3d(dvm_plan_s *P)
 {
     GainTables &g = P->g;
-    void *ptrs[] = {g.rec, g.aw, g.tw, g.lamhat, g.units, g.shat, g.that};
+    void *ptrs[] = {g.rec, g.aw, g.tw, g.lamhat, g.units, g.shat, g.that, g.fg_rec, g.fg_aw, g.fg_t2d};
     for (void *q : ptrs)
         if (q) cudaFree(q);
     g = GainTables{};
+}
+
+dvm_status_t interleave_pairs(dvm_plan_s *P, const double *f, int64_t f_stride, int64_t ncells, int64_t nodes,
+                              double2 *fI)
+{
+    LaunchScope ls(P, KC_ZERO);
+    k_interleave<<<1184, 256, 0, P->stream>>>(f, f_stride, ncells, nodes, fI);
+    DVM_CUDA(cudaGetLastError());
+    return DVM_OK;
+}
+
+dvm_status_t deinterleave_pairs(dvm_plan_s *P, const double2 *QI, int nchunks, int64_t npairs, int64_t ncells,
+                                int64_t nodes, double *Q, int64_t q_stride)
+{
+    LaunchScope ls(P, KC_REDUCE);
+    k_deinterleave<<<1184, 256, 0, P->stream>>>(QI, nchunks, npairs, ncells, nodes, Q, q_stride);
+    DVM_CUDA(cudaGetLastError());
+    return DVM_OK;
 }
 
 dvm_status_t collide_gain3d(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q, int64_t q_stride,

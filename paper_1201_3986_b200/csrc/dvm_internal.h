@@ -82,6 +82,8 @@ struct Workspace {
     size_t p2_scr_elems = 0, p2_part_elems = 0;
     double2 *sp_z = nullptr;        // spectral path: f̂ and the per-direction transform
     size_t sp_z_elems = 0;
+    double2 *fg_fhat = nullptr;     // FFT gain: f̂ of the cell pairs [pairs][nodes]
+    size_t fg_fhat_elems = 0;
 };
 
 }  // namespace dvm
@@ -108,6 +110,9 @@ struct GainTables {
     int maxitems2d = 0;       // 2D: work items of the longest line walk
     double *shat = nullptr;   // spectral path: [A_local][N^d] line-filter spectra (real)
     double *that = nullptr;   // spectral path: [A_local][N^d] perp-filter spectra (real)
+    int4 *fg_rec = nullptr;   // FFT gain: [A_local][3] (e, M), (u, 0), (w, 0)
+    double *fg_aw = nullptr;  // FFT gain: [A_local] a_e / N^3
+    double *fg_t2d = nullptr; // FFT gain: [A_local][N][N] plane-filter spectra T2D_e(p, q)
     size_t bytes = 0;
 };
 
@@ -143,7 +148,7 @@ struct dvm_plan_s {
     uint64_t launches = 0;
     size_t table_bytes = 0;
     bool profiling = false;
-    int path_mode = 0;      // evaluation path: 0 auto, 1 v1 orbit sweeps, 2 gain3d/pair2d when built, 3 spectral
+    int path_mode = 0;      // evaluation path: 0 auto, 1 v1 orbit sweeps, 2 gain3d/pair2d when built, 3 spectral, 4 FFT gain (3D N = 64)
     bool use_graphs = true; // time steppers replay one captured step (CUDA graph)
     cudaStream_t gstream = nullptr;      // plan-owned stream for graph capture/replay
     cudaEvent_t gev[2] = {nullptr, nullptr};
@@ -229,6 +234,7 @@ dvm_status_t reduce_slots(dvm_plan_s *P, double *Q, int64_t q_stride, const doub
 dvm_status_t build_loss(dvm_plan_s *P);
 dvm_status_t set_weights(dvm_plan_s *P, const double *a_box, const double *b_box);
 void free_weights(dvm_plan_s *P);
+dvm_status_t fft_forward_pairs(dvm_plan_s *P, const double *f, int64_t f_stride, int64_t ncells, double2 *out);
 dvm_status_t loss_init(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q, int64_t q_stride, int64_t ncells,
                        double2 *QI);
 dvm_status_t collide_spectral(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q, int64_t q_stride,
@@ -238,6 +244,13 @@ dvm_status_t build_pair2d(dvm_plan_s *P);
 dvm_status_t collide_pair2d(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q, int64_t q_stride,
                             int64_t ncells, bool *handled);
 void free_gain3d(dvm_plan_s *P);
+dvm_status_t interleave_pairs(dvm_plan_s *P, const double *f, int64_t f_stride, int64_t ncells, int64_t nodes,
+                              double2 *fI);
+dvm_status_t deinterleave_pairs(dvm_plan_s *P, const double2 *QI, int nchunks, int64_t npairs, int64_t ncells,
+                                int64_t nodes, double *Q, int64_t q_stride);
+// 3D gain by per-direction FFT filtering (dvm_fgain3d.cu)
+dvm_status_t collide_fgain3d(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q, int64_t q_stride,
+                             int64_t ncells, bool *handled);
 dvm_status_t collide_gain3d(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q, int64_t q_stride,
                             int64_t ncells, bool *handled);
 void free_workspace(dvm_plan_s *P);

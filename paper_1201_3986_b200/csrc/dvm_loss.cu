@@ -550,6 +550,39 @@ dvm_status_t set_weights(dvm_plan_s *P, const double *a_box, const double *b_box
     return DVM_OK;
 }
 
+// f̂ of cell pairs: out[p] = FFT_d(f_{2p} + i f_{2p+1}) (forward, unnormalised;
+// an odd tail cell is paired with zero).
+dvm_status_t fft_forward_pairs(dvm_plan_s *P, const double *f, int64_t f_stride, int64_t ncells, double2 *out)
+{
+    const int d = P->d;
+    int64_t nodes = 1;
+    for (int j = 0; j < d; ++j) nodes *= P->N;
+    const int64_t npairs = (ncells + 1) / 2;
+    const double2 *tw = P->wt.on ? P->wt.tw : P->g.tw;
+    constexpr int64_t kBatch = 64;  // pairs per launch (grid size)
+    for (int64_t p0 = 0; p0 < npairs; p0 += kBatch) {
+        const int64_t np = std::min(kBatch, npairs - p0);
+        for (int k = 0; k < d; ++k) {
+            FftArgs a = {};
+            a.d = d;
+            a.npairs = np;
+            a.tw = tw;
+            a.r_cells = ncells;
+            a.r_first = 2 * p0;
+            a.ax = d - 1 - k;
+            a.zin = out + p0 * nodes;
+            a.zout = out + p0 * nodes;
+            if (k == 0) {
+                a.r0 = f;
+                a.r_stride = f_stride;
+            }
+            dvm_status_t st = fft_dispatch(P, a);
+            if (st) return st;
+        }
+    }
+    return DVM_OK;
+}
+
 // Loss initialisation Q[c] := −f[c] Λ[c] for cells [0, ncells) (Λ = λ ⊛ f).
 dvm_status_t loss_init(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q, int64_t q_stride, int64_t ncells,
                        double2 *QI)

@@ -329,6 +329,41 @@ def test_gain3d_ragged_batches():
     _assert_parity(qb[4][pts], Qo[0], "gain3d ragged batch")
 
 
+@pytest.mark.parametrize("Nbar,Nt,cells", [(2, 5, 1), (1, 4, 2), (2, 14, 3), (3, 7, 5), (8, 14, 2)])
+def test_fgain3d_path_matches_frame_path(Nbar, Nt, cells):
+    """3D N = 64 gain by per-direction FFT filtering (dvm_set_path(4)) against the
+    frame-plane kernel (path 2) and the oracle on sampled nodes; ragged pair
+    counts and direction chunking (few cells) included."""
+    N = 64
+    f = np.random.default_rng(Nbar * 10 + cells).uniform(0.0, 1.0, size=(cells, N ** 3))
+    p = _plan(3, N, Nbar, Ntilde=Nt)
+    p.set_path(2)
+    q2 = _gpu(p, f)
+    p.set_path(4)
+    q4 = _gpu(p, f)
+    np.testing.assert_allclose(q4, q2, rtol=0, atol=1e-12 * np.abs(q2).max())
+    assert np.array_equal(q4, _gpu(p, f))  # repeated call: bitwise
+    pts = np.arange(0, N ** 3, N ** 3 // 61)
+    Qo, _, _ = oracle.collide(f[cells - 1], 3, N, Nbar, Nt, 8.0, points=pts)
+    _assert_parity(q4[cells - 1][pts], Qo[0], f"fgain3d N̄={Nbar} Ñ={Nt}", ref=np.abs(q2[cells - 1]).max())
+
+
+def test_fgain3d_direction_shards_sum_to_full():
+    """Direction-sharded plans (each rank a subset of lines) on the FFT gain path
+    sum to the full operator."""
+    N, Nbar, Nt = 64, 3, 7
+    f = np.random.default_rng(3).uniform(0.0, 1.0, size=(2, N ** 3))
+    p = _plan(3, N, Nbar, Ntilde=Nt)
+    p.set_path(4)
+    full = _gpu(p, f)
+    acc = np.zeros_like(full)
+    for r in range(3):
+        ps = _plan(3, N, Nbar, Ntilde=Nt, shard_rank=r, shard_world=3)
+        ps.set_path(4)
+        acc += _gpu(ps, f)
+    np.testing.assert_allclose(acc, full, rtol=0, atol=1e-12 * np.abs(full).max())
+
+
 @pytest.mark.parametrize("N,Nbar,Nt,cells", [(16, 4, 4, 1), (64, 8, 14, 3), (256, 16, 57, 1), (128, 5, 20, 2),
                                             (32, 7, 7, 5)])
 def test_pair2d_path_matches_orbit_path(N, Nbar, Nt, cells):
@@ -499,7 +534,7 @@ def test_weighted_errors_and_reset():
         p.set_weights(odd, None)
     np.testing.assert_array_equal(_gpu(p, f), q_default)  # rejected tables leave the plan unchanged
     p.set_weights(dvm_inputs.even_weights(2, 4, 1), None)
-    for path in (1, 2):
+    for path in (1, 2, 4):
         p.set_path(path)
         with pytest.raises(DvmError):
             _gpu(p, f)

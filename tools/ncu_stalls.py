@@ -6,7 +6,7 @@ import sys
 out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "source", "--csv", "--print-source=cuda,sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
-want = set(int(x) for x in sys.argv[2].split(",")) if len(sys.argv) > 2 else None
+want = set(int(x) for x in sys.argv[2].split(",")) if len(sys.argv) > 2 and sys.argv[2] else None
 hdr = None
 agg = {}
 for r in rows:
@@ -28,8 +28,13 @@ for r in rows:
                 a[h] = a.get(h, 0.0) + float(r[i] or 0)
             except ValueError:
                 pass
-for ln, a in sorted(agg.items()):
+order = sorted(agg.items())
+if len(sys.argv) > 3 and sys.argv[3] == "top":  # heaviest lines first
+    order = sorted(agg.items(), key=lambda kv: -sum(v for k, v in kv[1].items() if k != "src"))[:40]
+grand = sum(v for _, a in agg.items() for k, v in a.items() if k != "src") or 1
+for ln, a in order:
+    allv = sum(v for k, v in a.items() if k != "src")
     st = sorted(((v, k) for k, v in a.items() if k != "src" and v > 0), reverse=True)[:6]
     tot = sum(v for v, _ in st) or 1
-    print(f"{ln}: {a['src']}")
+    print(f"{ln}: [{100 * allv / grand:.1f}% of samples] {a['src']}")
     print("    " + ", ".join(f"{k[6:]}={100 * v / tot:.0f}%" for v, k in st))
