@@ -38,6 +38,7 @@ constexpr int FN2 = FN * FN;
 constexpr int64_t FNODES = (int64_t)FN * FN * FN;
 constexpr int FRS = FN + 1;      // padded row pitch of a plane in shared memory (double2)
 constexpr int FTP = FN + 1;      // padded row pitch of the T2D table (double)
+constexpr int FTR = FN / 2 + 1;  // rows of T2D kept in shared memory (the table is even: T(-p,-q) = T(p,q))
 constexpr int FMS = 32;          // tap table size (2 M_e <= 32)
 #ifndef FG_TAPLD
 #define FG_TAPLD ld2_nc_hint
@@ -62,8 +63,8 @@ struct FgArgs {
 
 struct FgSmem {
     static constexpr size_t xb = sizeof(double2) * 2 * FN * FRS;  // two plane buffers
-    static constexpr size_t t2 = sizeof(double) * FN * FTP;       // T2D_e of the step
-    static constexpr size_t rb = sizeof(double2) * FN * 32;       // phase-B ring stage / exchange
+    static constexpr size_t t2 = (sizeof(double) * FTR * FTP + 127) / 128 * 128;  // T2D_e of the step, rows 0..N/2
+    static constexpr size_t rb = sizeof(double2) * 2 * FN * 32;   // phase-B ring stage / exchange, 2 batches
     static constexpr size_t tw = sizeof(double2) * FN;            // W_64^k (inverse sign)
     static constexpr size_t total = xb + t2 + rb + tw;
 };
@@ -151,9 +152,9 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fgain3d(FgArgs A)
     constexpr int NBAT = 2 * FRY; // phase-B batches (one row y, 32 columns z)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double2 *xb = reinterpret_cast<double2 *>(smem_raw);                            // [2][FN][FRS]
-    double *t2 = reinterpret_cast<double *>(smem_raw + FgSmem::xb);                  // [FN][FTP]
-    double2 *rb = reinterpret_cast<double2 *>(smem_raw + FgSmem::xb + FgSmem::t2);   // [FN][32]
-    double2 *tw = rb + FN * 32;                                                      // [FN]
+    double *t2 = reinterpret_cast<double *>(smem_raw + FgSmem::xb);                  // [FTR][FTP]
+    double2 *rb = reinterpret_cast<double2 *>(smem_raw + FgSmem::xb + FgSmem::t2);   // [2][FN][32]
+    double2 *tw = rb + 2 * FN * 32;                                                  // [FN]
     __shared__ uint32_t soff[FMS];
     __shared__ int smB[4];
 
@@ -190,7 +191,7 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fgain3d(FgArgs A)
     // phase A loads: T2D_e (8-byte pieces into padded rows) and planes of f̂
     auto load_t2d = [&](int di) {
         const double *src = A.t2d + (int64_t)di * FN2;
-        for (int i = t; i < FN2; i += kRoleT) cp_async8(t2 + (i >> 6) * FTP + (i & 63), src + i);
+        for (int i = t; i < FTR * FN; i += kRoleT) cp_async8(t2 + (i >> 6) * FTP + (i & 63), src + i);
         cp_async_commit();
     };
     auto load_plane = [&](const double2 *fh, int g, double2 *dst) {
@@ -258,7 +259,10 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fgain3d(FgArgs A)
                             const int du = (8 * ru.z) & (FN - 1), dw = (8 * rw.z) & (FN - 1);
 #pragma unroll
                             for (int n2 = 0; n2 < 8; ++n2) {
-                                const double tv = t2[pu * FTP + pw];
+                                // rows p > N/2 from the even symmetry T(p, q) = T(N - p, N - q)
+                                const bool up = pu > FN / 2;
+                                const int tp = up ? FN - pu : pu, tq = up ? (FN - pw) & (FN - 1) : pw;
+                                const double tv = t2[tp * FTP + tq];
                                 const double2 x = X[r * FRS + n1 + 8 * n2];
                                 v[n2] = make_double2(x.x * tv, x.y * tv);
                                 pu = (pu + du) & (FN - 1);
@@ -336,10 +340,11 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fgain3d(FgArgs A)
                 // ring columns of batch b -> rb[ξ_x][lane] (warp w stages ξ_x = w + 8 j)
                 auto stage = [&](int b) {
                     const int y = FRY * rank + (b >> 1), z = 32 * (b & 1) + lane;
+                    double2 *R = rb + (b & 1) * FN * 32;
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
                         const int xi = warp + 8 * j;
-                        cp_async16_pol(rb + xi * 32 + lane, Tb + ((int64_t)xi * FN + y) * FN + z, drop);
+                        cp_async16_pol(R + xi * 32 + lane, Tb + ((int64_t)xi * FN + y) * FN + z, drop);
                     }
                     cp_async_commit();
                 };
@@ -348,8 +353,10 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fgain3d(FgArgs A)
                 for (int b = 0; b < ((A.dbg & 1) ? 0 : NBAT); ++b) {
                     const int y = FRY * rank + (b >> 1), z = 32 * (b & 1) + lane;
                     double2 v[8];
+                    double2 *R = rb + (b & 1) * FN * 32;
                     cp_async_wait_all();
-                    role_sync(bar);  // batch b staged (and soff written)
+                    role_sync(bar);  // batch b staged (and soff written); batch b-1's buffer is free
+                    if (b + 1 < NBAT) stage(b + 1);
                     if (!(A.dbg & 64)) {
                         // the staged ring lines are dead: drop them from L2 without a write-back
                         // (256 lines of 128 B per batch, one per thread)
@@ -359,20 +366,18 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fgain3d(FgArgs A)
                     {
                         const int n1 = warp;
 #pragma unroll
-                        for (int n2 = 0; n2 < 8; ++n2) v[n2] = rb[(n1 + 8 * n2) * 32 + lane];
+                        for (int n2 = 0; n2 < 8; ++n2) v[n2] = R[(n1 + 8 * n2) * 32 + lane];
                         idft8(v);
 #pragma unroll
                         for (int k2 = 1; k2 < 8; ++k2) v[k2] = cmul(v[k2], tw[(n1 * k2) & (FN - 1)]);
                         // back into the slots this thread read (ξ_x = n1 + 8 k2): no hazard
 #pragma unroll
-                        for (int k2 = 0; k2 < 8; ++k2) rb[(n1 + 8 * k2) * 32 + lane] = v[k2];
+                        for (int k2 = 0; k2 < 8; ++k2) R[(n1 + 8 * k2) * 32 + lane] = v[k2];
                     }
                     role_sync(bar);
                     const int k2 = warp;
 #pragma unroll
-                    for (int n1 = 0; n1 < 8; ++n1) v[n1] = rb[(n1 + 8 * k2) * 32 + lane];
-                    role_sync(bar);
-                    if (b + 1 < NBAT) stage(b + 1);
+                    for (int n1 = 0; n1 < 8; ++n1) v[n1] = R[(n1 + 8 * k2) * 32 + lane];
                     idft8(v);  // v[k1] = N^3 T_e(x = k2 + 8 k1, y, z)
 #pragma unroll
                     for (int hh = 0; hh < 2; ++hh) {

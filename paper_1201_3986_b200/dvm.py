@@ -14,7 +14,8 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdvm.so")
+# DVM_LIB: an alternative build of the same library (A/B timing in tools/)
+LIB_PATH = os.environ.get("DVM_LIB") or os.path.join(_HERE, "libdvm.so")
 
 DVM_MAXWELL_2D = 0
 DVM_HARD_SPHERES_3D = 1
