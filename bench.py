@@ -164,6 +164,15 @@ def run_reference(args):
     return 0
 
 
+# what limits the dominant kernel (ncu evidence in profiles/r01/SUMMARY.md)
+BINDING = {
+    "k_fgain3d": "latency-bound mix: SM L1/shared data pipe 58% (FFT exchanges, plane/ring staging, tap loads), "
+                 "fp64 pipe 22%, issue 31%; see profiles/r01/SUMMARY.md",
+    "k_gain3d": "SM L1/shared-memory pipe (sliding-program loads + scattered frame gather/store); "
+                "see profiles/r01/SUMMARY.md",
+}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -233,7 +242,7 @@ def run_ours(args):
     # (one f pass per direction + f read + Q write).  k_gain3d evaluates the
     # whole batch (all cells, all directions) in one launch per collide; the v1
     # orbit path launches k_rowsum once per direction chunk.
-    if top_name == "k_gain3d":
+    if top_name in ("k_gain3d", "k_fgain3d"):
         alg_bytes = (A + 2) * 8.0 * nodes * cells * psteps / top_n
     else:
         alg_bytes = (A + 2) * 8.0 * nodes * cells * psteps / max(1, prof.get("k_rowsum", (0, 1))[1])
@@ -253,8 +262,7 @@ def run_ours(args):
                 "peak_source": peak_src,
                 "note": "streaming-formulation bytes (A+2)*8*N^3 per cell-evaluation (SURVEY.md 8(d)); "
                         "effective, not DRAM traffic",
-                "binding_resource": "SM L1/shared-memory pipe (sliding-program loads + scattered frame "
-                                    "gather/store); see profiles/r01/SUMMARY.md"}
+                "binding_resource": BINDING.get(top_name, "see profiles/r01/SUMMARY.md")}
     eff_step_gbs = value / world * (A + 2) * 8.0 * nodes / 1e9
 
     # ---- e2e through the C ABI with host buffers (pinned), copies inside the timed region

@@ -509,7 +509,7 @@ dvm_status_t dvm_profile_enable(dvm_plan_t P, int enable)
 }
 
 static const char *kClassNames[] = {"k_linesum", "k_rowsum", "k_reduce", "k_zero", "k_moments", "k_axpy", "plan",
-                                    "k_gain3d", "k_fft"};
+                                    "k_gain3d", "k_fft", "k_fgain3d"};
 
 const char *dvm_profile_name(int k) { return (k >= 0 && k < KC_COUNT) ? kClassNames[k] : nullptr; }
 

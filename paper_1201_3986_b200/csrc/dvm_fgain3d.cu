@@ -575,7 +575,7 @@ dvm_status_t collide_fgain3d(dvm_plan_s *P, const double *f, int64_t f_stride, d
         fprintf(stderr, "[dvm] fgain3d: %d groups x %d CTAs, %d chunks, smem %zu\n", ngroups, CL, nchunks, smem);
     {
         void *args[] = {&a};
-        LaunchScope ls(P, KC_GAIN3D);
+        LaunchScope ls(P, KC_FGAIN3D);
         const cudaError_t le =
             cudaLaunchCooperativeKernel((void *)kern, dim3(ngroups * CL), dim3(2 * kRoleT), args, smem, P->stream);
         if (le == cudaErrorCooperativeLaunchTooLarge || le == cudaErrorNotSupported) {

@@ -89,7 +89,7 @@ struct Workspace {
 }  // namespace dvm
 
 namespace dvm {
-enum KernelClass { KC_LINESUM = 0, KC_ROWSUM, KC_REDUCE, KC_ZERO, KC_MOMENTS, KC_AXPY, KC_PLAN, KC_GAIN3D, KC_FFT, KC_COUNT };
+enum KernelClass { KC_LINESUM = 0, KC_ROWSUM, KC_REDUCE, KC_ZERO, KC_MOMENTS, KC_AXPY, KC_PLAN, KC_GAIN3D, KC_FFT, KC_FGAIN3D, KC_COUNT };
 struct ProfRec {
     int cls;
     cudaEvent_t a, b;
