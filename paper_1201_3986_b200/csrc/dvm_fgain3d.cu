@@ -537,9 +537,17 @@ dvm_status_t collide_fgain3d(dvm_plan_s *P, const double *f, int64_t f_stride, d
     if (getenv("DVM_G3_GROUPS")) max_groups = std::max(1, std::min(max_groups, atoi(getenv("DVM_G3_GROUPS"))));
     const int nloc = (int)P->local.size();
     const int64_t npairs = (ncells + 1) / 2;
+    // direction chunks per pair: the persistent groups take (pair, chunk) items round-robin;
+    // pick the fewest chunks whose busiest group does within 0.5 % of the balanced share
+    // (256 pairs on 9 groups: 2 chunks, 28.5 instead of 29 pair-times)
     int nchunks = 1;
-    if (npairs < max_groups) nchunks = (int)std::min<int64_t>(std::max(1, nloc), max_groups / npairs);
-    nchunks = std::max(1, nchunks);
+    {
+        auto rounds = [&](int c) { return (double)((npairs * c + max_groups - 1) / max_groups) / c; };
+        double best = 1e30;
+        const int cmax = (int)std::max<int64_t>(1, std::min<int64_t>(nloc, std::max<int64_t>(16, max_groups / npairs)));
+        for (int c = 1; c <= cmax; ++c) best = std::min(best, rounds(c));
+        while (nchunks < cmax && rounds(nchunks) > best * 1.005) ++nchunks;
+    }
     const int64_t items = npairs * nchunks;
     const int ngroups = (int)std::min<int64_t>(max_groups, items);
     Workspace &w = P->ws;
