@@ -16,8 +16,11 @@
 //     exchange per axis), write the plane to the group's ring slot.
 //   group progress counters (per CTA, monotonic)
 //   phase B (warps 8-15): CTA `rank` owns the rows y ∈ [4 rank, 4 rank + 4):
-//     inverse FFT along ξ_x of its 256 columns, then Q += a_e S_e T_e with
+//     ring columns loaded straight into registers one batch ahead, inverse FFT
+//     along ξ_x of its 256 columns, then Q += a_e S_e T_e with
 //     S_e = Σ_{1<=|m|<=M_e} f(.+me) read as coalesced taps; Q lives in TMEM.
+//   The roles run separate loops so setmaxnreg can move registers from A (88)
+//   to B (168).
 // Loss and the layout conversions are shared with dvm_gain3d.cu.
 #include <math.h>
 #include <stdio.h>
@@ -40,6 +43,7 @@ constexpr int FRS = FN + 1;      // padded row pitch of a plane in shared memory
 constexpr int FTP = FN + 1;      // padded row pitch of the T2D table (double)
 constexpr int FTR = FN / 2 + 1;  // rows of T2D kept in shared memory (the table is even: T(-p,-q) = T(p,q))
 constexpr int FMS = 32;          // tap table size (2 M_e <= 32)
+constexpr int kRegA = 88, kRegB = 168;  // setmaxnreg split of the 128 x 512 register file (A + B <= 256)
 #ifndef FG_TAPLD
 #define FG_TAPLD ld2_nc_hint
 #endif
@@ -64,7 +68,7 @@ struct FgArgs {
 struct FgSmem {
     static constexpr size_t xb = sizeof(double2) * 2 * FN * FRS;  // two plane buffers
     static constexpr size_t t2 = (sizeof(double) * FTR * FTP + 127) / 128 * 128;  // T2D_e of the step, rows 0..N/2
-    static constexpr size_t rb = sizeof(double2) * 2 * FN * 32;   // phase-B ring stage / exchange, 2 batches
+    static constexpr size_t rb = sizeof(double2) * 2 * FN * 32;   // phase-B x-FFT exchange, 2 batches
     static constexpr size_t tw = sizeof(double2) * FN;            // W_64^k (inverse sign)
     static constexpr size_t total = xb + t2 + rb + tw;
 };
@@ -206,6 +210,9 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fgain3d(FgArgs A)
         load_t2d((int)((int64_t)A.nloc * (grp % A.nchunks) / A.nchunks));
     }
 
+    if (roleA) {
+        // phase A fits in 88 registers; phase B takes the rest (register prefetch of the ring)
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegA));
     for (int64_t item = grp; item < items; item += ngroups) {
         const int64_t pair = item / A.nchunks;
         const int chunk = (int)(item % A.nchunks);
@@ -226,7 +233,7 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fgain3d(FgArgs A)
                 ndi = (int)((int64_t)A.nloc * ((item + ngroups) % A.nchunks) / A.nchunks);
                 fh_next = A.fhat + ((item + ngroups) / A.nchunks) * FNODES;
             }
-            if (roleA) {
+            {
                 // ============================================ phase A: planes of IFFT_yz(f̂ t̂_e)
                 // (T2D_e and the first plane are in flight since the previous step)
                 if (stepi >= (unsigned)A.slots) group_wait<CL>(cB, stepi - A.slots + 1, t, bar);
@@ -318,7 +325,32 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fgain3d(FgArgs A)
                     cur ^= 1;
                 }
                 role_signal(cA + rank, stepi + 1, leader, bar);
-            } else {
+            }
+        }
+    }
+    } else {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegB));
+    for (int64_t item = grp; item < items; item += ngroups) {
+        const int64_t pair = item / A.nchunks;
+        const int chunk = (int)(item % A.nchunks);
+        const int d0 = (int)((int64_t)A.nloc * chunk / A.nchunks);
+        const int d1 = (int)((int64_t)A.nloc * (chunk + 1) / A.nchunks);
+        const double2 *__restrict__ fh = A.fhat + pair * FNODES;
+        const double2 *__restrict__ fc = A.f + pair * FNODES;
+        double2 *Qc = A.Q + ((int64_t)chunk * A.npairs + pair) * FNODES;
+
+        for (int di = d0; di < d1; ++di, ++stepi) {
+            double2 *Tb = A.ring + ((int64_t)grp * A.slots + (stepi % A.slots)) * FNODES;
+            // the group's next step (direction, cell pair), -1 at the end
+            int ndi = -1;
+            const double2 *fh_next = fh;
+            if (di + 1 < d1) {
+                ndi = di + 1;
+            } else if (item + ngroups < items) {
+                ndi = (int)((int64_t)A.nloc * ((item + ngroups) % A.nchunks) / A.nchunks);
+                fh_next = A.fhat + ((item + ngroups) / A.nchunks) * FNODES;
+            }
+            {
                 // ============================================ phase B: IFFT_x, Q += a_e S_e T_e
                 if (t == 0) {
                     const int4 re = A.rec[(int64_t)di * 3];
@@ -337,42 +369,36 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fgain3d(FgArgs A)
                 const double aw = A.aw[di];
                 const int M2 = 2 * M;
                 const uint64_t keep = l2_keep(), drop = l2_drop();
-                // ring columns of batch b -> rb[ξ_x][lane] (warp w stages ξ_x = w + 8 j)
-                auto stage = [&](int b) {
+                // ring columns straight into registers, one batch ahead (coalesced 512 B per warp row)
+                double2 pre[8];
+                auto fetch = [&](int b) {
                     const int y = FRY * rank + (b >> 1), z = 32 * (b & 1) + lane;
-                    double2 *R = rb + (b & 1) * FN * 32;
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const int xi = warp + 8 * j;
-                        cp_async16_pol(R + xi * 32 + lane, Tb + ((int64_t)xi * FN + y) * FN + z, drop);
-                    }
-                    cp_async_commit();
+                    for (int n2 = 0; n2 < 8; ++n2) pre[n2] = ld2_cg_hint(Tb + ((int64_t)(warp + 8 * n2) * FN + y) * FN + z, drop);
                 };
-                if (!(A.dbg & 1)) stage(0);
+                if (!(A.dbg & 1)) fetch(0);
 #pragma unroll 1
                 for (int b = 0; b < ((A.dbg & 1) ? 0 : NBAT); ++b) {
                     const int y = FRY * rank + (b >> 1), z = 32 * (b & 1) + lane;
                     double2 v[8];
+                    // buffer of pass-1 outputs: batch b - 2 used it, every thread is past b - 1's barrier
                     double2 *R = rb + (b & 1) * FN * 32;
-                    cp_async_wait_all();
-                    role_sync(bar);  // batch b staged (and soff written); batch b-1's buffer is free
-                    if (b + 1 < NBAT) stage(b + 1);
-                    if (!(A.dbg & 64)) {
-                        // the staged ring lines are dead: drop them from L2 without a write-back
-                        // (256 lines of 128 B per batch, one per thread)
-                        const double2 *line = Tb + ((int64_t)(t >> 2) * FN + y) * FN + 32 * (b & 1) + 8 * (t & 3);
-                        asm volatile("discard.global.L2 [%0], 128;" ::"l"(line) : "memory");
-                    }
                     {
                         const int n1 = warp;
 #pragma unroll
-                        for (int n2 = 0; n2 < 8; ++n2) v[n2] = R[(n1 + 8 * n2) * 32 + lane];
+                        for (int n2 = 0; n2 < 8; ++n2) v[n2] = pre[n2];
+                        if (b + 1 < NBAT) fetch(b + 1);
                         idft8(v);
 #pragma unroll
                         for (int k2 = 1; k2 < 8; ++k2) v[k2] = cmul(v[k2], tw[(n1 * k2) & (FN - 1)]);
-                        // back into the slots this thread read (ξ_x = n1 + 8 k2): no hazard
 #pragma unroll
                         for (int k2 = 0; k2 < 8; ++k2) R[(n1 + 8 * k2) * 32 + lane] = v[k2];
+                    }
+                    if (!(A.dbg & 64)) {
+                        // the ring lines this warp read for batch b are dead (32 lines of 128 B, one per lane)
+                        __syncwarp();
+                        const double2 *line = Tb + ((int64_t)(warp + 8 * (lane >> 2)) * FN + y) * FN + 32 * (b & 1) + 8 * (lane & 3);
+                        asm volatile("discard.global.L2 [%0], 128;" ::"l"(line) : "memory");
                     }
                     role_sync(bar);
                     const int k2 = warp;
@@ -403,6 +429,10 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fgain3d(FgArgs A)
                         }
                         uint32_t r[16];
                         const uint32_t ta = tm_base + (uint32_t)(32 * b + 16 * hh);
+                        // the TMEM load and store are unconditional (.sync.aligned: every lane must
+                        // execute the same instruction; no data-dependent branch around them)
+                        __syncwarp();
+                        tmem_ld16(ta, r);
                         if (first) {
 #pragma unroll
                             for (int q = 0; q < 4; ++q) {
@@ -412,9 +442,6 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fgain3d(FgArgs A)
                                 r[4 * q + 2] = __double2loint(qv.y);
                                 r[4 * q + 3] = __double2hiint(qv.y);
                             }
-                        } else {
-                            __syncwarp();  // .sync.aligned: the warp must be converged
-                            tmem_ld16(ta, r);
                         }
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
@@ -423,19 +450,14 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fgain3d(FgArgs A)
                             double qy = __hiloint2double(r[4 * q + 3], r[4 * q + 2]);
                             qx += aw * T.x * S[q].x;
                             qy += aw * T.y * S[q].y;
-                            if (last) {
-                                st2_hint(Qc + n[q], make_double2(qx, qy), drop);
-                            } else {
-                                r[4 * q + 0] = __double2loint(qx);
-                                r[4 * q + 1] = __double2hiint(qx);
-                                r[4 * q + 2] = __double2loint(qy);
-                                r[4 * q + 3] = __double2hiint(qy);
-                            }
+                            if (last) st2_hint(Qc + n[q], make_double2(qx, qy), drop);
+                            r[4 * q + 0] = __double2loint(qx);
+                            r[4 * q + 1] = __double2hiint(qx);
+                            r[4 * q + 2] = __double2loint(qy);
+                            r[4 * q + 3] = __double2hiint(qy);
                         }
-                        if (!last) {
-                            __syncwarp();
-                            tmem_st16(ta, r);
-                        }
+                        __syncwarp();
+                        tmem_st16(ta, r);
                     }
                 }
                 __syncwarp();
@@ -443,6 +465,7 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fgain3d(FgArgs A)
                 role_signal(cB + rank, stepi + 1, leader, bar);
             }
         }
+    }
     }
     if (!roleA) {
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
