@@ -419,10 +419,13 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fgain3d(FgArgs A)
                         for (int k = 0; k < ((A.dbg & 4) ? 0 : M2); k += 2) {
                             const uint32_t o0 = soff[k], o1 = soff[k + 1];
                             double2 a[4], c[4];
+                            // the 4 nodes differ only in x (the top field, 8 q apart): one carry-less
+                            // add per tap, then plain adds modulo N^3 for the other nodes
+                            const uint32_t b0 = swar_add(n[0], o0, H2), b1 = swar_add(n[0], o1, H2);
 #pragma unroll
                             for (int q = 0; q < 4; ++q) {
-                                a[q] = FG_TAPLD(fc + swar_add(n[q], o0, H2), keep);
-                                c[q] = FG_TAPLD(fc + swar_add(n[q], o1, H2), keep);
+                                a[q] = FG_TAPLD(fc + ((b0 + (uint32_t)q * 8u * FN2) & (uint32_t)(FNODES - 1)), keep);
+                                c[q] = FG_TAPLD(fc + ((b1 + (uint32_t)q * 8u * FN2) & (uint32_t)(FNODES - 1)), keep);
                             }
 #pragma unroll
                             for (int q = 0; q < 4; ++q) S[q] = add2(S[q], add2(a[q], c[q]));
