@@ -184,7 +184,9 @@ DVM_API const char *dvm_profile_name(int k);
 /* Evaluation path: 0 = auto (default), 1 = v1 orbit sweeps only, 2 = the
  * FFT-loss paths whenever the plan built them, 4 = 3D N = 64: the gain by
  * per-direction FFT filtering (T_e of two cells from one inverse transform of
- * f̂ t̂_e, S_e as line taps; auto for 3D N = 64), 3 = the spectral reference
+ * f̂ t̂_e, S_e as line taps; auto for 3D N = 64; like 2, used whenever the
+ * plan supports it: the 3D kernels hold 2 M_e <= 32 taps, so plans with
+ * Ñ > 16 evaluate by the v1 sweeps), 3 = the spectral reference
  * path (per direction one inverse transform gives
  * S_e + i T_e from the real filter spectra; a second cross-check, slow:
  * A inverse FFTs per cell; its tables need 16 A N^d bytes, <= 4 GB).  The FFT-loss paths evaluate

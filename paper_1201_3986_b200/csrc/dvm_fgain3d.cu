@@ -543,6 +543,10 @@ dvm_status_t collide_fgain3d(dvm_plan_s *P, const double *f, int64_t f_stride, d
 {
     *handled = false;
     if (P->d != 3 || P->N != FN || !P->g.ready || ncells <= 0) return DVM_OK;
+    // the tap table holds 2 M_e <= 32 offsets (M_e <= Ñ): such plans have no 3D fast
+    // path (build_gain3d leaves g.ready unset) and are evaluated by the v1 sweeps
+    for (int di : P->local)
+        if (P->h_M[di] > FMS / 2) return DVM_OK;
     dvm_status_t st;
     if ((st = build_fg_tables(P))) return st;
     const int CL = getenv("DVM_FG_CL") ? atoi(getenv("DVM_FG_CL")) : 16;

@@ -545,6 +545,10 @@ dvm_status_t launch_gain(dvm_plan_s *P, const double *f, int64_t f_stride, doubl
 dvm_status_t build_gain3d(dvm_plan_s *P)
 {
     if (P->d != 3 || (P->N != 32 && P->N != 64)) return DVM_OK;
+    // line half-widths beyond the kernels' tap tables (Ñ > 16): no 3D fast path for this
+    // plan; the orbit sweeps (v1) and the spectral path evaluate it
+    for (int di : P->local)
+        if (P->h_M[di] > kMaxMS / 2) return DVM_OK;
     const int nloc = (int)P->local.size();
     const int N = P->N;
     const int L = N == 32 ? G3Geom<32>::SEGLEN : G3Geom<64>::SEGLEN;

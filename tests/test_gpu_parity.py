@@ -348,6 +348,23 @@ def test_fgain3d_path_matches_frame_path(Nbar, Nt, cells):
     _assert_parity(q4[cells - 1][pts], Qo[0], f"fgain3d N̄={Nbar} Ñ={Nt}", ref=np.abs(q2[cells - 1]).max())
 
 
+def test_fgain3d_large_ntilde_falls_back():
+    """Ñ > 16 exceeds the 3D kernels' tap tables (2 M_e <= 32): the plan still
+    builds and both auto mode and dvm_set_path(4) evaluate by the orbit sweeps
+    (bitwise the v1 path, parity with the oracle)."""
+    N, Nbar, Nt = 64, 2, 20
+    f = np.random.default_rng(7).uniform(0.0, 1.0, size=(2, N ** 3))
+    p = _plan(3, N, Nbar, Ntilde=Nt)
+    q = _gpu(p, f)
+    pts = np.arange(0, N ** 3, N ** 3 // 41)
+    Qo, _, _ = oracle.collide(f[1], 3, N, Nbar, Nt, 8.0, points=pts)
+    _assert_parity(q[1][pts], Qo[0], "auto, Ñ=20")
+    p.set_path(4)
+    q4 = _gpu(p, f)
+    p.set_path(1)
+    assert np.array_equal(q4, _gpu(p, f)) and np.array_equal(q, q4)
+
+
 def test_fgain3d_direction_shards_sum_to_full():
     """Direction-sharded plans (each rank a subset of lines) on the FFT gain path
     sum to the full operator."""
