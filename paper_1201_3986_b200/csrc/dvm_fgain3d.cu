@@ -43,6 +43,10 @@ constexpr int FRS = FN + 1;      // padded row pitch of a plane in shared memory
 constexpr int FTP = FN + 1;      // padded row pitch of the T2D table (double)
 constexpr int FTR = FN / 2 + 1;  // rows of T2D kept in shared memory (the table is even: T(-p,-q) = T(p,q))
 constexpr int FMS = 32;          // tap table size (2 M_e <= 32)
+#ifndef FG_TAPUNROLL
+#define FG_TAPUNROLL 1  // 8 loads in flight per tap pair; unrolling further measured slower
+#endif
+constexpr int kTapUnroll = FG_TAPUNROLL;
 constexpr int kRegA = 88, kRegB = 168;  // setmaxnreg split of the 128 x 512 register file (A + B <= 256)
 #ifndef FG_TAPLD
 #define FG_TAPLD ld2_nc_hint
@@ -142,7 +146,10 @@ __device__ __forceinline__ void group_wait(const unsigned int *ctrs, unsigned in
                 ok = v >= target;
             }
             if (__all_sync(0xffffffffu, ok)) break;
-            __nanosleep(32);
+#ifndef FG_SLEEP
+#define FG_SLEEP 32
+#endif
+            if (FG_SLEEP) __nanosleep(FG_SLEEP);
         }
     }
     role_sync(id);
@@ -415,7 +422,7 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fgain3d(FgArgs A)
                             S[q] = make_double2(0.0, 0.0);
                         }
                         // taps ±m e in pairs (M2 is even): 8 independent loads per iteration
-#pragma unroll 2
+#pragma unroll kTapUnroll
                         for (int k = 0; k < ((A.dbg & 4) ? 0 : M2); k += 2) {
                             const uint32_t o0 = soff[k], o1 = soff[k + 1];
                             double2 a[4], c[4];
