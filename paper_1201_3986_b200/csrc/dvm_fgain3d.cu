@@ -47,7 +47,11 @@ constexpr int FMS = 32;          // tap table size (2 M_e <= 32)
 #define FG_TAPUNROLL 1  // 8 loads in flight per tap pair; unrolling further measured slower
 #endif
 constexpr int kTapUnroll = FG_TAPUNROLL;
-constexpr int kRegA = 88, kRegB = 168;  // setmaxnreg split of the 128 x 512 register file (A + B <= 256)
+constexpr int kRegA = 88, kRegB = 168;
+#ifndef FG_TF_REGA
+#define FG_TF_REGA 96
+#endif
+constexpr int kRegATF = FG_TF_REGA, kRegBTF = 256 - FG_TF_REGA;  // TF: A holds 8 more TMEM words  // setmaxnreg split of the 128 x 512 register file (A + B <= 256)
 #ifndef FG_TAPLD
 #define FG_TAPLD ld2_nc_hint
 #endif
@@ -69,13 +73,15 @@ struct FgArgs {
                           // 4 skip the taps
 };
 
-struct FgSmem {
-    static constexpr size_t xb = sizeof(double2) * 2 * FN * FRS;  // two plane buffers
+template <bool TF>
+struct FgSmemT {
+    static constexpr size_t xb = sizeof(double2) * (TF ? 1 : 2) * FN * FRS;  // plane buffer(s)
     static constexpr size_t t2 = (sizeof(double) * FTR * FTP + 127) / 128 * 128;  // T2D_e of the step, rows 0..N/2
     static constexpr size_t rb = sizeof(double2) * 2 * FN * 32;   // phase-B x-FFT exchange, 2 batches
     static constexpr size_t tw = sizeof(double2) * FN;            // W_64^k (inverse sign)
     static constexpr size_t total = xb + t2 + rb + tw;
 };
+using FgSmem = FgSmemT<false>;
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b)
 {
@@ -132,6 +138,31 @@ __device__ __forceinline__ void cp_async8(void *smem_dst, const void *gsrc)
 }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
+// 32 columns of this thread's TMEM lane (8 double2)
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32])
+{
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32])
+{
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+        "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+        "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+        : "memory");
+}
+
 // progress counters of a group of CL CTAs (role_wait of dvm_g3common.h for CL <= 32)
 template <int CL>
 __device__ __forceinline__ void group_wait(const unsigned int *ctrs, unsigned int target, int t, int id)
@@ -155,16 +186,20 @@ __device__ __forceinline__ void group_wait(const unsigned int *ctrs, unsigned in
     role_sync(id);
 }
 
-template <int CL>
+// TF: f̂ of the group's cell pair resident in TMEM (groups of 32 CTAs: each CTA's 2
+// planes are 128 KB = TMEM columns 256-511; Q takes columns 0-255), no plane loads
+template <int CL, bool TF>
 __global__ void __launch_bounds__(2 * kRoleT, 1) k_fgain3d(FgArgs A)
 {
+    static_assert(!TF || CL == 32, "TMEM-resident f̂ needs 2 planes per CTA");
+    using Sm = FgSmemT<TF>;
     constexpr int FPL = FN / CL;  // ξ_x planes per CTA per direction
     constexpr int FRY = FN / CL;  // phase-B rows y per CTA
     constexpr int NBAT = 2 * FRY; // phase-B batches (one row y, 32 columns z)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double2 *xb = reinterpret_cast<double2 *>(smem_raw);                            // [2][FN][FRS]
-    double *t2 = reinterpret_cast<double *>(smem_raw + FgSmem::xb);                  // [FTR][FTP]
-    double2 *rb = reinterpret_cast<double2 *>(smem_raw + FgSmem::xb + FgSmem::t2);   // [2][FN][32]
+    double *t2 = reinterpret_cast<double *>(smem_raw + Sm::xb);                      // [FTR][FTP]
+    double2 *rb = reinterpret_cast<double2 *>(smem_raw + Sm::xb + Sm::t2);           // [2][FN][32]
     double2 *tw = rb + 2 * FN * 32;                                                  // [FN]
     __shared__ uint32_t soff[FMS];
     __shared__ int smB[4];
@@ -197,7 +232,10 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fgain3d(FgArgs A)
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t tm_base = roleA ? 0u : (s_tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(256 * (warp >> 2)));
+    // B: Q accumulators (64 or 32 node pairs per thread); A (TF): the f̂ planes
+    constexpr uint32_t QCOLS = TF ? 128 : 256;
+    const uint32_t tm_lane = s_tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+    const uint32_t tm_base = roleA ? (TF ? tm_lane + 256u + 128u * (warp >> 2) : 0u) : tm_lane + QCOLS * (warp >> 2);
 
     // phase A loads: T2D_e (8-byte pieces into padded rows) and planes of f̂
     auto load_t2d = [&](int di) {
@@ -212,22 +250,45 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fgain3d(FgArgs A)
         for (int i = t; i < FN2; i += kRoleT) cp_async16_pol(dst + (i >> 6) * FRS + (i & 63), src + i, pol);
         cp_async_commit();
     };
+    // TF: the planes ξ_x = rank + CL kp of a pair into this thread's TMEM columns,
+    // [kp][h][n2] x double2: exactly the row-pass inputs of thread (n1 = warp, r = lane + 32 h)
+    auto load_fhat_tmem = [&](const double2 *fh) {
+#pragma unroll 1
+        for (int kp = 0; kp < 2; ++kp)
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+                uint32_t r[32];
+                const double2 *src = fh + (int64_t)(rank + CL * kp) * FN2 + (lane + 32 * h) * FN + warp;
+#pragma unroll
+                for (int n2 = 0; n2 < 8; ++n2) {
+                    const double2 x = src[8 * n2];
+                    r[4 * n2 + 0] = __double2loint(x.x);
+                    r[4 * n2 + 1] = __double2hiint(x.x);
+                    r[4 * n2 + 2] = __double2loint(x.y);
+                    r[4 * n2 + 3] = __double2hiint(x.y);
+                }
+                __syncwarp();
+                tmem_st32(tm_base + 64u * kp + 32u * h, r);
+            }
+        tmem_wait_st();
+    };
     if (roleA && grp < items && !(A.dbg & 2)) {
-        load_plane(A.fhat + (grp / A.nchunks) * FNODES, rank, xb);
+        if constexpr (!TF) load_plane(A.fhat + (grp / A.nchunks) * FNODES, rank, xb);
         load_t2d((int)((int64_t)A.nloc * (grp % A.nchunks) / A.nchunks));
     }
 
     if (roleA) {
         // phase A fits in 88 registers; phase B takes the rest (register prefetch of the ring)
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegA));
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(TF ? kRegATF : kRegA));
     for (int64_t item = grp; item < items; item += ngroups) {
         const int64_t pair = item / A.nchunks;
         const int chunk = (int)(item % A.nchunks);
         const int d0 = (int)((int64_t)A.nloc * chunk / A.nchunks);
         const int d1 = (int)((int64_t)A.nloc * (chunk + 1) / A.nchunks);
         const double2 *__restrict__ fh = A.fhat + pair * FNODES;
-        const double2 *__restrict__ fc = A.f + pair * FNODES;
-        double2 *Qc = A.Q + ((int64_t)chunk * A.npairs + pair) * FNODES;
+        if constexpr (TF) {
+            if (!(A.dbg & 2)) load_fhat_tmem(fh);
+        }
 
         for (int di = d0; di < d1; ++di, ++stepi) {
             double2 *Tb = A.ring + ((int64_t)grp * A.slots + (stepi % A.slots)) * FNODES;
@@ -251,16 +312,23 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fgain3d(FgArgs A)
                 for (int kp = 0; kp < ((A.dbg & 2) ? 0 : FPL); ++kp) {
                     const int g = rank + kp * CL;
                     const bool lastp = kp + 1 == FPL;
-                    if (!lastp) {
-                        load_plane(fh, g + CL, xb + (cur ^ 1) * FN * FRS);
-                        cp_async_wait1();
+                    if constexpr (TF) {
+                        if (kp == 0) {
+                            cp_async_wait_all();  // T2D_e of this step
+                            role_sync(bar);
+                        }
                     } else {
-                        cp_async_wait_all();
+                        if (!lastp) {
+                            load_plane(fh, g + CL, xb + (cur ^ 1) * FN * FRS);
+                            cp_async_wait1();
+                        } else {
+                            cp_async_wait_all();
+                        }
+                        role_sync(bar);
+                        // the last plane: the next step's first plane goes into the other buffer
+                        if (lastp && ndi >= 0) load_plane(fh_next, rank, xb + (cur ^ 1) * FN * FRS);
                     }
-                    role_sync(bar);
-                    // the last plane: the next step's first plane goes into the other buffer
-                    if (lastp && ndi >= 0) load_plane(fh_next, rank, xb + (cur ^ 1) * FN * FRS);
-                    double2 *X = xb + cur * FN * FRS;
+                    double2 *X = xb + (TF ? 0 : cur) * FN * FRS;
                     double2 v[8];
                     // --- rows: t̂ multiply, inverse FFT along ξ_z (four-step 8 × 8)
 #pragma unroll 1
@@ -271,13 +339,23 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fgain3d(FgArgs A)
                             int pu = (ru.x * g + ru.y * r + ru.z * n1) & (FN - 1);
                             int pw = (rw.x * g + rw.y * r + rw.z * n1) & (FN - 1);
                             const int du = (8 * ru.z) & (FN - 1), dw = (8 * rw.z) & (FN - 1);
+                            uint32_t fr[TF ? 32 : 1];
+                            if constexpr (TF) {
+                                __syncwarp();
+                                tmem_ld32(tm_base + 64u * kp + 32u * h, fr);
+                            }
 #pragma unroll
                             for (int n2 = 0; n2 < 8; ++n2) {
                                 // rows p > N/2 from the even symmetry T(p, q) = T(N - p, N - q)
                                 const bool up = pu > FN / 2;
                                 const int tp = up ? FN - pu : pu, tq = up ? (FN - pw) & (FN - 1) : pw;
                                 const double tv = t2[tp * FTP + tq];
-                                const double2 x = X[r * FRS + n1 + 8 * n2];
+                                double2 x;
+                                if constexpr (TF)
+                                    x = make_double2(__hiloint2double(fr[4 * n2 + 1], fr[4 * n2]),
+                                                     __hiloint2double(fr[4 * n2 + 3], fr[4 * n2 + 2]));
+                                else
+                                    x = X[r * FRS + n1 + 8 * n2];
                                 v[n2] = make_double2(x.x * tv, x.y * tv);
                                 pu = (pu + du) & (FN - 1);
                                 pw = (pw + dw) & (FN - 1);
@@ -285,7 +363,7 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fgain3d(FgArgs A)
                             idft8(v);
 #pragma unroll
                             for (int k2 = 1; k2 < 8; ++k2) v[k2] = cmul(v[k2], tw[(n1 * k2) & (FN - 1)]);
-                            role_sync(bar);
+                            if constexpr (!TF) role_sync(bar);  // other warps still read the staged plane
 #pragma unroll
                             for (int k2 = 0; k2 < 8; ++k2) X[r * FRS + 8 * k2 + ((n1 + k2) & 7)] = v[k2];
                         }
@@ -336,7 +414,7 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fgain3d(FgArgs A)
         }
     }
     } else {
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegB));
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(TF ? kRegBTF : kRegB));
     for (int64_t item = grp; item < items; item += ngroups) {
         const int64_t pair = item / A.nchunks;
         const int chunk = (int)(item % A.nchunks);
@@ -556,13 +634,15 @@ dvm_status_t collide_fgain3d(dvm_plan_s *P, const double *f, int64_t f_stride, d
         if (P->h_M[di] > FMS / 2) return DVM_OK;
     dvm_status_t st;
     if ((st = build_fg_tables(P))) return st;
-    const int CL = getenv("DVM_FG_CL") ? atoi(getenv("DVM_FG_CL")) : 16;
+    // DVM_FG_TMEM=1: groups of 32 CTAs with f̂ resident in TMEM (k_fgain3d<32, true>)
+    const bool tf = getenv("DVM_FG_TMEM") && atoi(getenv("DVM_FG_TMEM")) != 0;
+    const int CL = tf ? 32 : (getenv("DVM_FG_CL") ? atoi(getenv("DVM_FG_CL")) : 16);
     if (CL != 16 && CL != 32) {
         set_error("DVM_FG_CL must be 16 or 32");
         return DVM_E_UNSUPPORTED;
     }
-    auto kern = CL == 16 ? k_fgain3d<16> : k_fgain3d<32>;
-    const size_t smem = FgSmem::total;
+    auto kern = tf ? k_fgain3d<32, true> : (CL == 16 ? k_fgain3d<16, false> : k_fgain3d<32, false>);
+    const size_t smem = tf ? FgSmemT<true>::total : FgSmemT<false>::total;
     DVM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int dev = 0, sms = 0, per_sm = 0, coop = 0;
     DVM_CUDA(cudaGetDevice(&dev));
