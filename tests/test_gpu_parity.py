@@ -348,6 +348,20 @@ def test_fgain3d_path_matches_frame_path(Nbar, Nt, cells):
     _assert_parity(q4[cells - 1][pts], Qo[0], f"fgain3d N̄={Nbar} Ñ={Nt}", ref=np.abs(q2[cells - 1]).max())
 
 
+def test_fgain3d_chunked_rounds_match_frame_path():
+    """A batch with more pairs than groups and several direction chunks per pair
+    (20 cells = 10 pairs on 9 groups: the chunk rule picks more than one chunk
+    and the groups take several rounds) equals the frame-plane path; c5 inputs."""
+    f = dvm_inputs.make("c5", cells=20)
+    p = _plan(3, 64, 8)
+    p.set_path(2)
+    q2 = _gpu(p, f)
+    p.set_path(4)
+    q4 = _gpu(p, f)
+    np.testing.assert_allclose(q4, q2, rtol=0, atol=1e-12 * np.abs(q2).max())
+    assert np.array_equal(q4, _gpu(p, f))
+
+
 def test_fgain3d_large_ntilde_falls_back():
     """Ñ > 16 exceeds the 3D kernels' tap tables (2 M_e <= 32): the plan still
     builds and both auto mode and dvm_set_path(4) evaluate by the orbit sweeps
