@@ -56,7 +56,12 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b)
 template <int N>
 __global__ void __launch_bounds__(kFT) k_fft_pass(FftArgs A)
 {
-    constexpr int B = (1024 / N) < N ? (1024 / N) : N;
+#ifndef FFT_B256
+#define FFT_B256 1
+#endif
+    // lines per CTA: 16 KB tiles, but one line for N = 256 (a 2D cell has only 256 lines:
+    // 256 CTAs instead of 64; c3 loss 50 -> 35 us, measured B = 4 / 2 / 1)
+    constexpr int B = N == 256 ? FFT_B256 : ((1024 / N) < N ? (1024 / N) : N);
     constexpr int LOGN = N == 16 ? 4 : N == 32 ? 5 : N == 64 ? 6 : N == 128 ? 7 : 8;
     __shared__ double2 buf[B * N];
     const int d = A.d, ax = A.ax;
