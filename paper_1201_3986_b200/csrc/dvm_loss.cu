@@ -53,15 +53,20 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b)
 // One radix-2 FFT pass of length N along axis `ax` for every line of every
 // pair in the batch.  Tile = B lines (contiguous rows for the last axis,
 // lines adjacent in the last axis otherwise).
-template <int N>
-__global__ void __launch_bounds__(kFT) k_fft_pass(FftArgs A)
-{
 #ifndef FFT_B256
 #define FFT_B256 1
 #endif
-    // lines per CTA: 16 KB tiles, but one line for N = 256 (a 2D cell has only 256 lines:
-    // 256 CTAs instead of 64; c3 loss 50 -> 35 us, measured B = 4 / 2 / 1)
-    constexpr int B = N == 256 ? FFT_B256 : ((1024 / N) < N ? (1024 / N) : N);
+// lines per CTA (the kernel's tile and the launcher's grid): 16 KB tiles, but fewer
+// lines for N = 256 (a 2D cell has only 256 lines: more CTAs per pass)
+__host__ __device__ constexpr int fft_lines_per_cta(int N)
+{
+    return N == 256 ? FFT_B256 : ((1024 / N) < N ? (1024 / N) : N);
+}
+
+template <int N>
+__global__ void __launch_bounds__(kFT) k_fft_pass(FftArgs A)
+{
+    constexpr int B = fft_lines_per_cta(N);
     constexpr int LOGN = N == 16 ? 4 : N == 32 ? 5 : N == 64 ? 6 : N == 128 ? 7 : 8;
     __shared__ double2 buf[B * N];
     const int d = A.d, ax = A.ax;
@@ -240,7 +245,7 @@ __global__ void k_take_real(const double2 *z, int64_t n, double *out)
 template <int N>
 dvm_status_t fft_pass(dvm_plan_s *P, const FftArgs &a)
 {
-    constexpr int B = (1024 / N) < N ? (1024 / N) : N;
+    constexpr int B = fft_lines_per_cta(N);
     int64_t nodes = 1;
     for (int j = 0; j < a.d; ++j) nodes *= N;
     const int64_t tiles = a.npairs * (nodes / N / B);
