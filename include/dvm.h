@@ -186,7 +186,11 @@ DVM_API const char *dvm_profile_name(int k);
  * per-direction FFT filtering (T_e of two cells from one inverse transform of
  * f̂ t̂_e, S_e as line taps; auto for 3D N = 64; like 2, used whenever the
  * plan supports it: the 3D kernels hold 2 M_e <= 32 taps, so plans with
- * Ñ > 16 evaluate by the v1 sweeps), 3 = the spectral reference
+ * Ñ > 16 evaluate by the v1 sweeps), 5 = 2D with N <= 64 (auto there): one
+ * CTA per direction pair {e, e⊥} and cell holds f in shared memory and
+ * evaluates gain and loss of the pair with direct line windows (the loss as
+ * f [a (Box − W_e⊥) + a (Box − W_e)], Box the 2D window), partials summed in
+ * pair order (two launches, no FFT), 3 = the spectral reference
  * path (per direction one inverse transform gives
  * S_e + i T_e from the real filter spectra; a second cross-check, slow:
  * A inverse FFTs per cell; its tables need 16 A N^d bytes, <= 4 GB).  The FFT-loss paths evaluate

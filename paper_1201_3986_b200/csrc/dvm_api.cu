@@ -540,9 +540,9 @@ dvm_status_t dvm_set_path(dvm_plan_t P, int path)
         set_error("NULL argument");
         return DVM_E_NULL;
     }
-    if (path < 0 || path > 4) {
-        set_error("path must be 0 (auto), 1 (v1 orbit sweeps), 2 (gain3d / pair2d), 3 (spectral reference) or 4 "
-                  "(3D FFT gain)");
+    if (path < 0 || path > 5) {
+        set_error("path must be 0 (auto), 1 (v1 orbit sweeps), 2 (gain3d / pair2d), 3 (spectral reference), 4 "
+                  "(3D FFT gain) or 5 (2D small grids)");
         return DVM_E_STATE;
     }
     P->path_mode = path;

@@ -368,6 +368,12 @@ dvm_status_t collide_batched(dvm_plan_s *P, const double *f, double *Q, int64_t 
         dvm_status_t st = collide_fgain3d(P, f, stride, Q, stride, ncells, &handled);
         if (st || handled) return st;
     }
+    // auto for 2D N <= 64: pair units with the loss per pair, f in shared memory (two launches)
+    if (P->path_mode == 5 || (P->path_mode == 0 && P->d == 2 && P->N <= 64)) {
+        bool handled = false;
+        dvm_status_t st = collide_small2d(P, f, stride, Q, stride, ncells, &handled);
+        if (st || handled) return st;
+    }
     const bool use_new = P->path_mode == 2 || P->path_mode == 4 || (P->path_mode == 0 && (P->d == 3 || P->N >= 128));
     if (use_new) {
         bool handled = false;

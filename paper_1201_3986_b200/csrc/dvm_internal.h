@@ -241,6 +241,8 @@ dvm_status_t collide_spectral(dvm_plan_s *P, const double *f, int64_t f_stride, 
                               int64_t ncells);
 dvm_status_t build_gain3d(dvm_plan_s *P);
 dvm_status_t build_pair2d(dvm_plan_s *P);
+dvm_status_t collide_small2d(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q, int64_t q_stride,
+                             int64_t ncells, bool *handled);
 dvm_status_t collide_pair2d(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q, int64_t q_stride,
                             int64_t ncells, bool *handled);
 void free_gain3d(dvm_plan_s *P);

@@ -176,7 +176,116 @@ __global__ void k_sum_units(const double *__restrict__ part, int nunits, int nce
     }
 }
 
+// ---- small grids (N <= 64): one CTA per (pair unit, cell) holds f and W_B in shared
+// memory; the loss is evaluated per pair as well (no FFT):
+//   U_A = Σ_{1<=|m|<=M} T_A(x + m A) = Box − W_B,  U_B = Box − W_A,
+//   Box(x) = Σ_{|m|,|n| <= M} f(x + m A + n B)  (the window of W_B along A),
+//   part_u = ca (W_A − f) W_B + cb (W_B − f) W_A − f [ca (Box − W_B) + cb (Box − W_A)]
+// with ca = a [A local], cb = a [B local] (eq:decD with β̃ = β − β(L,L), PAPER.md:545,
+// 822-831; in 2D the perp set of A is the line of B).  Direct
+// window sums from shared memory (2M+1 loads each); partials summed in unit order.
+#ifndef S2_THREADS
+#define S2_THREADS 1024  // c2: 256 threads 40 us, 512 31 us, 1024 29 us
+#endif
+constexpr int kST = S2_THREADS;
+
+__global__ void __launch_bounds__(kST) k_small2d(const double *__restrict__ f, int64_t f_stride,
+                                                const Unit2D *__restrict__ units, int nunits, int p,
+                                                double *__restrict__ part)
+{
+    extern __shared__ double sm2[];
+    const int N = 1 << p, mask = N - 1;
+    const int nodes = N * N;
+    double *F = sm2, *WB = sm2 + nodes;
+    const int u = blockIdx.x, c = blockIdx.y;
+    const Unit2D U = units[u];
+    const double *fc = f + (int64_t)c * f_stride;
+    for (int i = threadIdx.x; i < nodes; i += kST) F[i] = fc[i];
+    __syncthreads();
+    const int M = U.M;
+    // W_B(x) = Σ_{|m| <= M} f(x + m B)
+    for (int i = threadIdx.x; i < nodes; i += kST) {
+        const int x0 = i >> p, x1 = i & mask;
+        double w = 0.0;
+        for (int m = -M; m <= M; ++m) w += F[(((x0 + m * U.b0) & mask) << p) | ((x1 + m * U.b1) & mask)];
+        WB[i] = w;
+    }
+    __syncthreads();
+    const double ca = (U.flags & 1) ? U.aw : 0.0, cb = (U.flags & 2) ? U.aw : 0.0;
+    double *out = part + ((int64_t)c * nunits + u) * nodes;
+    for (int i = threadIdx.x; i < nodes; i += kST) {
+        const int x0 = i >> p, x1 = i & mask;
+        double wa = 0.0, box = 0.0;
+        for (int m = -M; m <= M; ++m) {
+            const int j = (((x0 + m * U.a0) & mask) << p) | ((x1 + m * U.a1) & mask);
+            wa += F[j];
+            box += WB[j];
+        }
+        const double f0 = F[i], wb = WB[i];
+        out[i] = ca * (wa - f0) * wb + cb * (wb - f0) * wa - f0 * (ca * (box - wb) + cb * (box - wa));
+    }
+}
+
+// Q[c][x] = Σ_u part[c][u][x], u ascending
+__global__ void k_small2d_sum(const double *__restrict__ part, int nunits, int ncells, int nodes,
+                              double *__restrict__ Q, int64_t q_stride)
+{
+    const int64_t total = (int64_t)ncells * nodes;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = i / nodes, x = i % nodes;
+        const double *pc = part + c * nunits * (int64_t)nodes + x;
+        double acc = 0.0;
+        for (int uu = 0; uu < nunits; ++uu) acc += pc[(int64_t)uu * nodes];
+        Q[c * q_stride + x] = acc;
+    }
+}
+
 }  // namespace
+
+// small 2D grids (N <= 64): gain and loss per pair unit in shared memory, two launches
+dvm_status_t collide_small2d(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q, int64_t q_stride,
+                             int64_t ncells, bool *handled)
+{
+    *handled = false;
+    if (P->d != 2 || P->N > 64 || !P->g.ready || ncells <= 0) return DVM_OK;
+    *handled = true;
+    const int N = P->N, p = P->p;
+    const int nodes = N * N;
+    const int nunits = P->g.nunits;
+    Workspace &w = P->ws;
+    dvm_status_t st;
+    if (nunits == 0) {
+        LaunchScope ls(P, KC_ZERO);
+        for (int64_t c = 0; c < ncells; ++c) DVM_CUDA(cudaMemsetAsync(Q + c * q_stride, 0, sizeof(double) * nodes, P->stream));
+        return DVM_OK;
+    }
+    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>({ncells, 65535, (int64_t)((256ull << 20) / (sizeof(double) * (uint64_t)nunits * nodes))}));
+    if ((st = grow(&w.p2_part, &w.p2_part_elems, (size_t)(chunk * nunits * nodes), P->stream))) return st;
+    const size_t smem = sizeof(double) * 2 * nodes;
+    static bool attr_set = false;  // the 64 KB opt-in, once per process (host time of small calls)
+    if (!attr_set) {
+        DVM_CUDA(cudaFuncSetAttribute(k_small2d, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(sizeof(double) * 2 * 64 * 64)));
+        attr_set = true;
+    }
+    const Unit2D *units = reinterpret_cast<const Unit2D *>(P->g.units);
+    for (int64_t c0 = 0; c0 < ncells; c0 += chunk) {
+        const int nc = (int)std::min<int64_t>(chunk, ncells - c0);
+        {
+            LaunchScope ls(P, KC_ROWSUM);
+            k_small2d<<<dim3(nunits, nc), kST, smem, P->stream>>>(f + c0 * f_stride, f_stride, units, nunits, p,
+                                                                  w.p2_part);
+        }
+        {
+            LaunchScope ls(P, KC_REDUCE);
+            const int64_t tot = (int64_t)nc * nodes;
+            k_small2d_sum<<<(unsigned)std::min<int64_t>(592, (tot + 255) / 256), 256, 0, P->stream>>>(
+                w.p2_part, nunits, nc, nodes, Q + c0 * q_stride, q_stride);
+        }
+        DVM_CUDA(cudaGetLastError());
+    }
+    return DVM_OK;
+}
 
 // Plan-time: pair units of the (local) directions, loss tables.
 dvm_status_t build_pair2d(dvm_plan_s *P)

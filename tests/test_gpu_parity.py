@@ -413,6 +413,24 @@ def test_pair2d_path_matches_orbit_path(N, Nbar, Nt, cells):
     _assert_parity(q2[-1][pts], Qo[0], f"pair2d N={N}", ref=np.abs(q1[-1]).max())
 
 
+@pytest.mark.parametrize("N,Nbar,Nt,cells", [(16, 4, 4, 1), (16, 2, 7, 3), (32, 5, 7, 2), (64, 8, 14, 3), (64, 3, 20, 1)])
+def test_small2d_path_matches_orbit_path(N, Nbar, Nt, cells):
+    """2D small grids (dvm_set_path 5, auto for N <= 64): gain and loss per pair
+    unit from shared memory (loss as f [a (Box − W_B) + a (Box − W_A)]) against
+    the v1 orbit sweeps and the oracle; ragged batches, M up to 20."""
+    f = np.random.default_rng(3 * N + cells).uniform(0.0, 1.0, size=(cells, N ** 2))
+    p = _plan(2, N, Nbar, Ntilde=Nt)
+    p.set_path(5)
+    q5 = _gpu(p, f)
+    assert np.array_equal(q5, _gpu(p, f))
+    p.set_path(1)
+    q1 = _gpu(p, f)
+    np.testing.assert_allclose(q5, q1, rtol=0, atol=1e-13 * np.abs(q1).max())
+    Qo, _, _ = oracle.collide(f[-1], 2, N, Nbar, Nt, 8.0)
+    _assert_parity(q5[-1], Qo, f"small2d N={N}")
+    assert abs(q5[-1].sum()) <= 1e-13 * np.abs(q5[-1]).sum()  # mass, per pair exactly
+
+
 # ---------------------------------------------------------------- time steppers (CUDA graphs)
 @pytest.mark.parametrize("d,N,Nbar,Nt,path", [(2, 64, 8, 14, 0), (2, 64, 8, 14, 2), (3, 32, 2, 5, 0)])
 def test_stepper_graph_replay_is_bitwise(d, N, Nbar, Nt, path):
