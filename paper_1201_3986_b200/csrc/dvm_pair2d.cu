@@ -190,14 +190,15 @@ __global__ void k_sum_units(const double *__restrict__ part, int nunits, int nce
 constexpr int kST = S2_THREADS;
 
 __global__ void __launch_bounds__(kST) k_small2d(const double *__restrict__ f, int64_t f_stride,
-                                                const Unit2D *__restrict__ units, int nunits, int p,
+                                                const Unit2D *__restrict__ units, int nunits, int nslice, int p,
                                                 double *__restrict__ part)
 {
     extern __shared__ double sm2[];
     const int N = 1 << p, mask = N - 1;
     const int nodes = N * N;
     double *F = sm2, *WB = sm2 + nodes;
-    const int u = blockIdx.x, c = blockIdx.y;
+    // CTA (unit u, slice s): W_B over the whole grid, the partial on slice s of the nodes
+    const int u = blockIdx.x / nslice, sl = blockIdx.x % nslice, c = blockIdx.y;
     const Unit2D U = units[u];
     const double *fc = f + (int64_t)c * f_stride;
     for (int i = threadIdx.x; i < nodes; i += kST) F[i] = fc[i];
@@ -213,7 +214,8 @@ __global__ void __launch_bounds__(kST) k_small2d(const double *__restrict__ f, i
     __syncthreads();
     const double ca = (U.flags & 1) ? U.aw : 0.0, cb = (U.flags & 2) ? U.aw : 0.0;
     double *out = part + ((int64_t)c * nunits + u) * nodes;
-    for (int i = threadIdx.x; i < nodes; i += kST) {
+    const int i0 = (int)((int64_t)nodes * sl / nslice), i1 = (int)((int64_t)nodes * (sl + 1) / nslice);
+    for (int i = i0 + threadIdx.x; i < i1; i += kST) {
         const int x0 = i >> p, x1 = i & mask;
         double wa = 0.0, box = 0.0;
         for (int m = -M; m <= M; ++m) {
@@ -235,6 +237,8 @@ __global__ void k_small2d_sum(const double *__restrict__ part, int nunits, int n
         const int64_t c = i / nodes, x = i % nodes;
         const double *pc = part + c * nunits * (int64_t)nodes + x;
         double acc = 0.0;
+        // unrolled so the loads are in flight together; the adds stay in unit order
+#pragma unroll 8
         for (int uu = 0; uu < nunits; ++uu) acc += pc[(int64_t)uu * nodes];
         Q[c * q_stride + x] = acc;
     }
@@ -269,12 +273,20 @@ dvm_status_t collide_small2d(dvm_plan_s *P, const double *f, int64_t f_stride, d
         attr_set = true;
     }
     const Unit2D *units = reinterpret_cast<const Unit2D *>(P->g.units);
+    int sms = 148;
+    {
+        int dev = 0;
+        DVM_CUDA(cudaGetDevice(&dev));
+        DVM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    }
     for (int64_t c0 = 0; c0 < ncells; c0 += chunk) {
         const int nc = (int)std::min<int64_t>(chunk, ncells - c0);
+        // node slices per unit so that one wave covers the SMs (the widest windows dominate)
+        const int nslice = (int)std::max<int64_t>(1, std::min<int64_t>(8, sms / ((int64_t)nunits * nc)));
         {
             LaunchScope ls(P, KC_ROWSUM);
-            k_small2d<<<dim3(nunits, nc), kST, smem, P->stream>>>(f + c0 * f_stride, f_stride, units, nunits, p,
-                                                                  w.p2_part);
+            k_small2d<<<dim3(nunits * nslice, nc), kST, smem, P->stream>>>(f + c0 * f_stride, f_stride, units,
+                                                                           nunits, nslice, p, w.p2_part);
         }
         {
             LaunchScope ls(P, KC_REDUCE);
