@@ -26,10 +26,12 @@ __device__ __forceinline__ void role_sync(int id) { asm volatile("bar.sync %0, %
 // own monotonic counter (ctrs[0..kCL)): lanes of the role's first warp poll one
 // counter each (acquire), then the role syncs.  Per-CTA counters, not a sum:
 // a CTA running ahead must not stand in for a slower one.
+template <int CL = kCL>
 __device__ __forceinline__ void role_wait(const unsigned int *ctrs, unsigned int target, int t, int id)
 {
+    static_assert(CL <= 32, "one polling lane per CTA");
     if (t < 32) {
-        bool ok = t >= kCL;
+        bool ok = t >= CL;
         for (;;) {
             if (!ok) {
                 unsigned int v;

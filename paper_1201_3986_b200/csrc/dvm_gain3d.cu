@@ -65,7 +65,7 @@ constexpr int kSlots = 2;   // T ring depth per group (phase A may run kSlots-1 
 // consecutive β-steps address rows r0 .. r0 + L - 1 without wrap logic.  The
 // raw plane is double-buffered: the next plane is gathered by cp.async while
 // the current one is scanned and evaluated.
-template <int N>
+template <int N, int CL = kCL>
 struct G3Geom {
     static constexpr int LOGN = N == 32 ? 5 : 6;
     static constexpr int SEGS = kRoleT / N;              // β segments per column
@@ -75,7 +75,7 @@ struct G3Geom {
     static constexpr int ROWS = N + L;
     static constexpr int RS = N + 1;
     static constexpr int PL = ROWS * RS;
-    static constexpr int NPL = N / kCL;                  // planes per CTA per direction
+    static constexpr int NPL = N / CL;                   // planes per CTA per direction
     static constexpr size_t smem = sizeof(double2) * (3 * (size_t)PL + ROWS) + sizeof(int4) * 2 * kMaxRec +
                                    sizeof(uint32_t) * 2 * kMaxMS;
 };
@@ -105,16 +105,17 @@ __device__ __forceinline__ void gather_plane(const double2 *fcp, double2 *dst, i
     cp_async_commit();
 }
 
-template <int N>
+template <int N, int CL>
 __global__ void __launch_bounds__(2 * kRoleT, 1) k_gain3d(GainArgs A)
 {
-    using Gm = G3Geom<N>;
+    using Gm = G3Geom<N, CL>;
     constexpr int LOGN = Gm::LOGN;
     constexpr int64_t NODES = (int64_t)N * N * N;
     constexpr int SEGLEN = Gm::SEGLEN;
     constexpr int L = Gm::L;
     constexpr int NCH = Gm::NCH;
-    constexpr int NPR = (int)(NODES / kCL);  // phase-B nodes per CTA
+    constexpr int NPR = (int)(NODES / CL);  // phase-B nodes per CTA
+    static_assert(4 * (NPR / kRoleT) <= 256, "phase-B accumulators exceed the thread's 256 TMEM columns");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int RS = Gm::RS;
     constexpr int NPL = Gm::NPL;
@@ -130,11 +131,11 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_gain3d(GainArgs A)
     const int lane = t & 31, warp = t >> 5;
     const bool leader = t == 0;
     const int bar = roleA ? 1 : 2;
-    const int rank = (int)(blockIdx.x % kCL);
-    const int grp = (int)(blockIdx.x / kCL);
-    const int ngroups = (int)(gridDim.x / kCL);
+    const int rank = (int)(blockIdx.x % CL);
+    const int grp = (int)(blockIdx.x / CL);
+    const int ngroups = (int)(gridDim.x / CL);
     const uint32_t H2 = A.H;
-    unsigned int *cA = A.ctr + (size_t)grp * 2 * kCL, *cB = cA + kCL;
+    unsigned int *cA = A.ctr + (size_t)grp * 2 * CL, *cB = cA + CL;
     unsigned int stepi = 0;
     const int64_t items = A.npairs * A.nchunks;
 
@@ -196,7 +197,7 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_gain3d(GainArgs A)
             if (roleA) {
                 // ============================================ phase A: T_e -> slot
                 if (ndi >= 0 && t < recw) rnext = A.rec[(int64_t)ndi * recw + t];
-                if (stepi >= kSlots) role_wait(cB, stepi - kSlots + 1, t, bar);
+                if (stepi >= kSlots) role_wait<CL>(cB, stepi - kSlots + 1, t, bar);
                 const int *smA = reinterpret_cast<const int *>(srec + buf * kMaxRec);
                 const int4 *sprog = srec + buf * kMaxRec + 6;
                 const int z0 = smA[3], z1 = smA[4], z2 = smA[5];
@@ -210,13 +211,13 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_gain3d(GainArgs A)
                 const double2 *fnext = (di + 1 < d1) ? fc : A.f + ((item + ngroups) / A.nchunks) * NODES;
 #pragma unroll 1
                 for (int kp = 0; kp < NPL; ++kp) {
-                    const int g = rank + kp * kCL;
+                    const int g = rank + kp * CL;
                     cp_async_wait_all();
                     role_sync(bar);  // plane g is in rawb[cur] (and the next record is visible)
                     if (A.dbg & 8) {
                         // timing experiment: no gather (T on stale data)
                     } else if (kp + 1 < NPL)
-                        gather_plane<N>(fc, rawb + (cur ^ 1) * Gm::PL, g + kCL, smA + 3, t, H2);
+                        gather_plane<N>(fc, rawb + (cur ^ 1) * Gm::PL, g + CL, smA + 3, t, H2);
                     else if (ndi >= 0)
                         gather_plane<N>(fnext, rawb + (cur ^ 1) * Gm::PL, rank,
                                         reinterpret_cast<const int *>(srec + (buf ^ 1) * kMaxRec) + 3, t, H2);
@@ -345,7 +346,7 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_gain3d(GainArgs A)
                         bnext3 = A.rec[(int64_t)ndi * recw + 3];
                     }
                 }
-                role_wait(cA, stepi + 1, t, bar);
+                role_wait<CL>(cA, stepi + 1, t, bar);
                 const int M = smB[3];
                 if (t < 2 * M) {
                     const int m = t / 2 + 1, sg = (t & 1) ? -1 : 1;
@@ -461,7 +462,15 @@ dvm_status_t launch_gain(dvm_plan_s *P, const double *f, int64_t f_stride, doubl
                          int64_t ncells, bool *fallback)
 {
     *fallback = false;
-    auto kern = k_gain3d<N>;
+    // CTAs per group: 16 (N = 64); N = 32 defaults to groups of 8 (more groups walk the
+    // directions in parallel; measured on c4), DVM_G3_CL overrides
+    int CL = N == 32 ? 8 : 16;
+    if (N == 32 && getenv("DVM_G3_CL")) CL = atoi(getenv("DVM_G3_CL"));
+    if (!(CL == 16 || (N == 32 && (CL == 8 || CL == 4)))) {
+        set_error("DVM_G3_CL (N = 32): 16, 8 or 4");
+        return DVM_E_UNSUPPORTED;
+    }
+    auto kern = CL == 16 ? k_gain3d<N, 16> : CL == 8 ? k_gain3d<N, (N == 32 ? 8 : 16)> : k_gain3d<N, (N == 32 ? 4 : 16)>;
     const size_t smem = gain_smem_bytes(N);
     DVM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int dev = 0, sms = 0, per_sm = 0, coop = 0;
@@ -473,7 +482,7 @@ dvm_status_t launch_gain(dvm_plan_s *P, const double *f, int64_t f_stride, doubl
         *fallback = true;
         return DVM_OK;
     }
-    int max_groups = (sms * per_sm) / kCL;
+    int max_groups = (sms * per_sm) / CL;
     if (getenv("DVM_G3_GROUPS")) max_groups = std::max(1, std::min(max_groups, atoi(getenv("DVM_G3_GROUPS"))));
     const int nloc = (int)P->local.size();
     const int64_t nodes = (int64_t)N * N * N;
@@ -488,7 +497,7 @@ dvm_status_t launch_gain(dvm_plan_s *P, const double *f, int64_t f_stride, doubl
     if ((st = grow(&w.g3_f, &w.g3_f_elems, (size_t)(npairs * nodes), P->stream))) return st;
     if ((st = grow(&w.g3_q, &w.g3_q_elems, (size_t)(nchunks * npairs * nodes), P->stream))) return st;
     if ((st = grow(&w.g3_t, &w.g3_t_elems, (size_t)ngroups * kSlots * nodes, P->stream))) return st;
-    if ((st = grow(&w.g3_ctr, &w.g3_ctr_elems, (size_t)ngroups * 2 * kCL, P->stream))) return st;
+    if ((st = grow(&w.g3_ctr, &w.g3_ctr_elems, (size_t)ngroups * 2 * CL, P->stream))) return st;
     {
         LaunchScope ls(P, KC_ZERO);
         k_interleave<<<1184, 256, 0, P->stream>>>(f, f_stride, ncells, nodes, w.g3_f);
@@ -499,7 +508,7 @@ dvm_status_t launch_gain(dvm_plan_s *P, const double *f, int64_t f_stride, doubl
                                  P->stream));
     // loss first: chunk 0 := −f Λ (interleaved)
     if ((st = loss_init(P, f, f_stride, nullptr, 0, ncells, w.g3_q))) return st;
-    DVM_CUDA(cudaMemsetAsync(w.g3_ctr, 0, sizeof(unsigned int) * 2 * kCL * ngroups, P->stream));
+    DVM_CUDA(cudaMemsetAsync(w.g3_ctr, 0, sizeof(unsigned int) * 2 * CL * ngroups, P->stream));
     GainArgs a;
     a.f = w.g3_f;
     a.Q = w.g3_q;
@@ -514,13 +523,13 @@ dvm_status_t launch_gain(dvm_plan_s *P, const double *f, int64_t f_stride, doubl
     a.H = P->pk.H;
     a.dbg = getenv("DVM_G3_DEBUG") ? atoi(getenv("DVM_G3_DEBUG")) : 0;
     if (getenv("DVM_VERBOSE"))
-        fprintf(stderr, "[dvm] gain3d N=%d: %d groups x %d CTAs, %d chunks, smem %zu\n", N, ngroups, kCL, nchunks,
+        fprintf(stderr, "[dvm] gain3d N=%d: %d groups x %d CTAs, %d chunks, smem %zu\n", N, ngroups, CL, nchunks,
                 smem);
     {
         void *args[] = {&a};
         LaunchScope ls(P, KC_GAIN3D);
         const cudaError_t le =
-            cudaLaunchCooperativeKernel((void *)kern, dim3(ngroups * kCL), dim3(2 * kRoleT), args, smem, P->stream);
+            cudaLaunchCooperativeKernel((void *)kern, dim3(ngroups * CL), dim3(2 * kRoleT), args, smem, P->stream);
         if (le == cudaErrorCooperativeLaunchTooLarge || le == cudaErrorNotSupported) {
             // the co-residency the group barriers need is not available now (e.g.
             // SMs held by another context): evaluate with the v1 sweeps instead
