@@ -1,6 +1,9 @@
 #!/bin/bash
-# c3 (2D N=256) device time per evaluation for several builds (tools/ab/libdvm_<name>.so)
-for n in "$@"; do echo -n "$n: "; DVM_LIB=tools/ab/libdvm_$n.so python - <<'PY'
+# c3 device time per evaluation under env variations ("-" = none)
+for spec in "$@"; do
+  [ "$spec" = "-" ] && spec=""
+  echo -n "== $spec: "
+  env $spec python - <<'PY'
 import sys, torch; sys.path.insert(0,'.')
 import dvm_inputs
 from paper_1201_3986_b200 import Plan
