@@ -8,6 +8,7 @@ computes one by one (27/9 nodes around argmax f + seeded uniform nodes), plus
 invariants that hold at any size.
 """
 import itertools
+import os
 import math
 
 import numpy as np
@@ -156,6 +157,18 @@ def test_parity_fuzz(seed):
 
 
 # ---------------------------------------------------------------- parity, BASELINE sizes (sampled)
+@pytest.mark.parametrize("name", ["c4", "c3"])
+def test_parity_full_grid_3d_and_c3(name):
+    """c4 (32^3) and c3 (256^2) on every node against the full direct oracle
+    (3.4e9 / 8.1e9 pair evaluations on the host cores: seconds), default path."""
+    cfg = dvm_inputs.CONFIGS[name]
+    f = dvm_inputs.make(name)
+    p = _plan(cfg.d, cfg.N, cfg.Nbar)
+    Qg = _gpu(p, f)[0]
+    Qo, _, _ = oracle.collide(f, cfg.d, cfg.N, cfg.Nbar, p.Ntilde, cfg.L)
+    _assert_parity(Qg, Qo[0], f"{name} full grid")
+
+
 @pytest.mark.parametrize("name,npts", [("c3", 1500), ("c4", 3000)])
 def test_parity_sampled_single_grid(name, npts):
     cfg = dvm_inputs.CONFIGS[name]
@@ -182,6 +195,22 @@ def test_parity_c5_sampled_batched():
         _assert_parity(Qg[c][pts], Qo[0], f"c5 cell {c}")
     sums = Qg.sum(axis=1)
     assert np.all(np.abs(sums) <= 1e-12 * np.abs(Qg).sum(axis=1))
+
+
+@pytest.mark.skipif(os.environ.get("DVM_FULL_C5") != "1", reason="7 min of host oracle time: DVM_FULL_C5=1")
+def test_parity_c5_full_cell_in_bench_launch():
+    """c5 as bench.py launches it (512 cells, one batched call, k_fgain3d with
+    direction chunks): the last cell on all 64^3 nodes against the full direct
+    oracle (4.2e11 pair evaluations: ~7 min on 16 host cores, so opt-in; result
+    in profiles/r01/c5_full_cell_parity.txt)."""
+    cfg = dvm_inputs.CONFIGS["c5"]
+    f = dvm_inputs.make("c5")
+    p = _plan(3, cfg.N, cfg.Nbar)
+    Qg = _gpu(p, f)
+    c = f.shape[0] - 1
+    Qo, _, _ = oracle.collide(f[c], 3, cfg.N, cfg.Nbar, p.Ntilde, cfg.L)
+    rel = _assert_parity(Qg[c], Qo[0], "c5 cell 511, all nodes")
+    print(f"c5 cell {c}, all {cfg.N ** 3} nodes: max |Q_gpu - Q_oracle| / max |Q_oracle| = {rel:.3e}")
 
 
 # ---------------------------------------------------------------- trajectories, invariants
