@@ -197,7 +197,8 @@ DVM_API const char *dvm_profile_name(int k);
  * the loss as one FFT convolution f (λ ⊛ f) (reading R21): 3D with N in
  * {32, 64}: gain by the frame-plane kernel (two cells per node,
  * warp-specialised, TMEM accumulators); 2D with 16 <= N <= 256: gain by
- * direction pairs {e, e⊥}.  Auto picks them for 3D and for 2D N >= 128, path 5
+ * direction pairs {e, e⊥}.  Auto picks them for 3D, for 2D N >= 256 and for
+ * N = 128 with >= 100 directions, path 5
  * for 2D 16 <= N <= 64, v1 otherwise.  All paths compute the same
  * operator; results agree to rounding (the FFT loss pairs cells in one complex
  * transform, so a cell's last bits may depend on its batch partner; a repeated

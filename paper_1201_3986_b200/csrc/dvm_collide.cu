@@ -374,7 +374,10 @@ dvm_status_t collide_batched(dvm_plan_s *P, const double *f, double *Q, int64_t 
         dvm_status_t st = collide_small2d(P, f, stride, Q, stride, ncells, &handled);
         if (st || handled) return st;
     }
-    const bool use_new = P->path_mode == 2 || P->path_mode == 4 || (P->path_mode == 0 && (P->d == 3 || P->N >= 128));
+    // auto: the 2D pair kernels from N = 256, and at N = 128 once there are >= 100 directions
+    // (tools/path128.py: N = 128 with N̄ = 7 (A = 72) v1 96 us vs 117, N̄ = 10 (A = 128) 131 vs 120)
+    const bool pair_auto = P->N >= 256 || (P->N >= 128 && P->A >= 100);
+    const bool use_new = P->path_mode == 2 || P->path_mode == 4 || (P->path_mode == 0 && (P->d == 3 || pair_auto));
     if (use_new) {
         bool handled = false;
         dvm_status_t st = P->d == 3 ? collide_gain3d(P, f, stride, Q, stride, ncells, &handled)
