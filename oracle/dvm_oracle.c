@@ -174,14 +174,19 @@ static int64_t orc_pairs(int d, int Ntilde, int Nbar, double h, int ndirs, const
     int64_t box = 1;
     for (int j = 0; j < d; ++j) box *= side;
     double hd1 = pow(h, d + 1);
-    int64_t n = 0;
-    int k[ORC_MAXD], l[ORC_MAXD];
-    for (int64_t ck = 0; ck < box; ++ck) {
-        int64_t r = ck;
+    /* the box points in lexicographic order, decoded once */
+    int *boxv = (int *)malloc(sizeof(int) * (size_t)(box * d));
+    if (!boxv) return -1;
+    for (int64_t c = 0; c < box; ++c) {
+        int64_t r = c;
         for (int j = d - 1; j >= 0; --j) {
-            k[j] = (int)(r % side) - Ntilde;
+            boxv[c * d + j] = (int)(r % side) - Ntilde;
             r /= side;
         }
+    }
+    int64_t n = 0;
+    for (int64_t ck = 0; ck < box; ++ck) {
+        const int *k = boxv + ck * d;
         if (!orc_k_allowed(d, k, Nbar, ndirs, dirs)) continue;
         int g = orc_gcd_vec(d, k);
         double norm = 0.0;
@@ -189,11 +194,7 @@ static int64_t orc_pairs(int d, int Ntilde, int Nbar, double h, int ndirs, const
         double a = hd1 * sqrt(norm) / (double)g; /* a(k) = h^{d+1}|k|/gcd(k) */
         if (wa) a = wa[orc_box_index(d, Ntilde, k)];
         for (int64_t cl = 0; cl < box; ++cl) {
-            int64_t s = cl;
-            for (int j = d - 1; j >= 0; --j) {
-                l[j] = (int)(s % side) - Ntilde;
-                s /= side;
-            }
+            const int *l = boxv + cl * d;
             long dot = 0;
             for (int j = 0; j < d; ++j) dot += (long)k[j] * l[j];
             if (dot != 0) continue; /* 1(k.l) */
@@ -207,6 +208,7 @@ static int64_t orc_pairs(int d, int Ntilde, int Nbar, double h, int ndirs, const
             ++n;
         }
     }
+    free(boxv);
     return n;
 }
 
@@ -226,30 +228,38 @@ static inline void neu_add(double *s, double *c, double x)
     *s = t;
 }
 
-static inline int64_t orc_wrap_index(int d, int N, const int *x, const int *o)
+/* Periodic index of node x + o (reading R10) from per-node
+ * tables: wrap[j][o_j + 2Ñ] = ((x_j + o_j) mod N) * N^{d-1-j}, filled once per
+ * node for every offset |o_j| <= 2Ñ (k, l and k + l all lie in [-2Ñ,2Ñ]^d).
+ * The table is only a precomputed "mod N"; the floating-point work and its
+ * order are those of the sum written above. */
+#define ORC_MAXW (4 * 64 + 1) /* 4Ñ + 1 entries per axis; Ñ <= 64 */
+#define ORC_NB 16               /* nodes evaluated side by side per pass over the pair list */
+static inline int64_t orc_wrap_index(int d, const int32_t (*wrap)[ORC_MAXW], int twoNt, const int *o)
 {
     int64_t idx = 0;
-    for (int j = 0; j < d; ++j) {
-        int c = (x[j] + o[j]) % N;
-        if (c < 0) c += N;
-        idx = idx * N + c;
-    }
+    for (int j = 0; j < d; ++j) idx += wrap[j][o[j] + twoNt];
     return idx;
 }
 
 /* Step 2.  Evaluate Q (and diagnostics G, Lo) at npts nodes of every cell
  * (npts < 0: all N^d nodes in storage order; otherwise pts[] holds node
- * indices).  Outputs are [ncells][npts]; any of Q, G, Lo may be NULL.
+ * indices, the same npts for every cell, or with pts_per_cell = 1 a
+ * [ncells][npts] table of each cell's own nodes).  Outputs are
+ * [ncells][npts]; any of Q, G, Lo may be NULL (G = Lo = NULL skips the
+ * diagnostics; Q is accumulated the same way either way).
  * h = 2L/N (reading R3).  ndirs < 0: all lines of order <= N̄; otherwise only
  * the given canonical lines.  wa/wb: optional box tables of a(k), b(l)
  * (see orc_pairs).  Returns 0 on success, negative on bad input. */
 int dvm_oracle_collide_w(int d, int N, int Nbar, int Ntilde, double L, const double *f,
-                         int64_t ncells, int64_t npts, const int64_t *pts, int ndirs,
+                         int64_t ncells, int64_t npts, const int64_t *pts, int pts_per_cell, int ndirs,
                          const int *dirs, const double *wa, const double *wb, double *Q, double *G,
                          double *Lo, int nthreads)
 {
     if (d < 1 || d > ORC_MAXD || N < 1 || Ntilde < 0 || ncells < 0 || !f) return -1;
+    { int64_t nn = 1; for (int j = 0; j < d; ++j) nn *= N; if (nn > 2147483647) return -1; } /* int32 node tables */
     if (npts >= 0 && npts > 0 && !pts) return -1;
+    if (4 * Ntilde + 1 > ORC_MAXW) return -1;
     double h = 2.0 * L / (double)N;
     int64_t cap = orc_pairs(d, Ntilde, Nbar, h, ndirs, dirs, wa, wb, 0, NULL, NULL, NULL);
     if (cap < 0) return -2;
@@ -273,32 +283,66 @@ int dvm_oracle_collide_w(int d, int N, int Nbar, int Ntilde, double L, const dou
 #else
     (void)nthreads;
 #endif
-#pragma omp parallel for schedule(dynamic, 16)
-    for (int64_t t = 0; t < total; ++t) {
-        int64_t cell = t / nout;
-        int64_t node = npts < 0 ? (t % nout) : pts[t % nout];
-        const double *fc = f + cell * nodes;
-        int x[ORC_MAXD];
-        int64_t r = node;
-        for (int j = d - 1; j >= 0; --j) {
-            x[j] = (int)(r % N);
-            r /= N;
+    const int twoNt = 2 * Ntilde;
+    /* Work items are blocks of ORC_NB consecutive outputs: the pair list is read
+     * once per block and applied to each node of the block in turn.  Every node
+     * still accumulates its own terms in pair-list order with its own
+     * compensated sums, so each result is exactly that of a one-node loop
+     * (the blocking only saves re-reading the list from memory). */
+    int64_t nblocks = (total + ORC_NB - 1) / ORC_NB;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t blk = 0; blk < nblocks; ++blk) {
+        int64_t t0 = blk * ORC_NB;
+        int nb = (int)(total - t0 < ORC_NB ? total - t0 : ORC_NB);
+        int32_t wrap[ORC_NB][ORC_MAXD][ORC_MAXW];
+        const double *fcs[ORC_NB];
+        double fi[ORC_NB];
+        double qs[ORC_NB], qc[ORC_NB], gs[ORC_NB], gc[ORC_NB], ls[ORC_NB], lc[ORC_NB];
+        for (int b = 0; b < nb; ++b) {
+            int64_t t = t0 + b;
+            int64_t cell = t / nout;
+            int64_t node = npts < 0 ? (t % nout) : (pts_per_cell ? pts[t] : pts[t % nout]);
+            const double *fc = f + cell * nodes;
+            int x[ORC_MAXD];
+            int64_t r = node;
+            for (int j = d - 1; j >= 0; --j) {
+                x[j] = (int)(r % N);
+                r /= N;
+            }
+            int64_t stride = 1;
+            for (int j = d - 1; j >= 0; --j) {
+                for (int o = -twoNt; o <= twoNt; ++o) {
+                    int c = (x[j] + o) % N;
+                    if (c < 0) c += N;
+                    wrap[b][j][o + twoNt] = (int32_t)(c * stride);
+                }
+                stride *= N;
+            }
+            fcs[b] = fc;
+            fi[b] = fc[node];
+            qs[b] = qc[b] = gs[b] = gc[b] = ls[b] = lc[b] = 0.0;
         }
-        double fi = fc[node];
-        double qs = 0.0, qc = 0.0, gs = 0.0, gc = 0.0, ls = 0.0, lc = 0.0;
+        const int diag = G || Lo;
         for (int64_t p = 0; p < cap; ++p) {
-            double fk = fc[orc_wrap_index(d, N, x, k + p * d)];
-            double fl = fc[orc_wrap_index(d, N, x, l + p * d)];
-            double fkl = fc[orc_wrap_index(d, N, x, kl + p * d)];
-            double gain = a[p] * (fk * fl);
-            double loss = a[p] * fkl;
-            neu_add(&qs, &qc, a[p] * (fk * fl - fi * fkl));
-            neu_add(&gs, &gc, gain);
-            neu_add(&ls, &lc, loss);
+            const int *kp = k + p * d, *lp = l + p * d, *klp = kl + p * d;
+            for (int b = 0; b < nb; ++b) {
+                const int32_t(*w)[ORC_MAXW] = (const int32_t(*)[ORC_MAXW])wrap[b];
+                double fk = fcs[b][orc_wrap_index(d, w, twoNt, kp)];
+                double fl = fcs[b][orc_wrap_index(d, w, twoNt, lp)];
+                double fkl = fcs[b][orc_wrap_index(d, w, twoNt, klp)];
+                neu_add(&qs[b], &qc[b], a[p] * (fk * fl - fi[b] * fkl));
+                if (diag) {
+                    neu_add(&gs[b], &gc[b], a[p] * (fk * fl)); /* gain */
+                    neu_add(&ls[b], &lc[b], a[p] * fkl);       /* loss (times f_i below) */
+                }
+            }
         }
-        if (Q) Q[t] = qs + qc;
-        if (G) G[t] = gs + gc;
-        if (Lo) Lo[t] = fi * (ls + lc);
+        for (int b = 0; b < nb; ++b) {
+            int64_t t = t0 + b;
+            if (Q) Q[t] = qs[b] + qc[b];
+            if (G) G[t] = gs[b] + gc[b];
+            if (Lo) Lo[t] = fi[b] * (ls[b] + lc[b]);
+        }
     }
     free(k);
     free(l);
@@ -311,6 +355,6 @@ int dvm_oracle_collide(int d, int N, int Nbar, int Ntilde, double L, const doubl
                        int64_t ncells, int64_t npts, const int64_t *pts, int ndirs,
                        const int *dirs, double *Q, double *G, double *Lo, int nthreads)
 {
-    return dvm_oracle_collide_w(d, N, Nbar, Ntilde, L, f, ncells, npts, pts, ndirs, dirs, NULL, NULL, Q, G,
-                                Lo, nthreads);
+    return dvm_oracle_collide_w(d, N, Nbar, Ntilde, L, f, ncells, npts, pts, 0, ndirs, dirs, NULL, NULL, Q,
+                                G, Lo, nthreads);
 }

@@ -57,7 +57,7 @@ def lib():
             L.dvm_oracle_collide.restype = ctypes.c_int
             L.dvm_oracle_collide_w.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                                ctypes.c_double, ctypes.c_void_p, ctypes.c_int64,
-                                               ctypes.c_int64, ctypes.c_void_p, ctypes.c_int,
+                                               ctypes.c_int64, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                                ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                                ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                                ctypes.c_int]
@@ -100,30 +100,42 @@ def _dirs_arg(dirs, d):
 
 def collide(f: np.ndarray, d: int, N: int, Nbar: int, Ntilde: int, L: float = 8.0,
             points: np.ndarray | None = None, dirs: np.ndarray | None = None,
-            nthreads: int = 0, a_box: np.ndarray | None = None, b_box: np.ndarray | None = None):
+            nthreads: int = 0, a_box: np.ndarray | None = None, b_box: np.ndarray | None = None,
+            diagnostics: bool = True):
     """Direct-sum Q, G, Lo for f of shape [cells, N^d] (or [N]*d / [cells]+[N]*d).
 
-    points: optional node indices (row-major) -> outputs [cells, npts];
+    points: optional node indices (row-major) -> outputs [cells, npts]; a 1-D
+    array is used for every cell, a [cells, npts] array gives each cell its own;
     dirs: optional subset of canonical lines (direction-sharding tests);
     a_box, b_box: optional general decoupled weights a(k), b(l) (eq:decoup,
     PAPER.md:575-579) tabulated over [-Ñ,Ñ]^d (shape [2Ñ+1]*d, index k + Ñ);
     Γ̃_{k,l} = a(k) b(l) replaces h^{d+1}|k|/gcd(k) (a_box None: that default;
     b_box None: b = 1).
+    diagnostics: False skips G and Lo (returned as None); Q is unchanged.
     Returns (Q, G, Lo) as float64 arrays of shape [cells, npts or N^d].
     """
     nodes = N ** d
     fa = np.ascontiguousarray(np.asarray(f, dtype=np.float64).reshape(-1, nodes))
     ncells = fa.shape[0]
+    per_cell = 0
     if points is None:
         npts, pp, pk = -1, None, None
         nout = nodes
     else:
-        pk = np.ascontiguousarray(np.asarray(points, dtype=np.int64).reshape(-1))
-        npts, pp = pk.shape[0], pk.ctypes.data
+        pk = np.asarray(points, dtype=np.int64)
+        if pk.ndim == 2:
+            if pk.shape[0] != ncells:
+                raise ValueError("per-cell points must have shape [cells, npts]")
+            per_cell = 1
+            npts = pk.shape[1]
+        else:
+            npts = pk.size
+        pk = np.ascontiguousarray(pk.reshape(-1))
+        pp = pk.ctypes.data
         nout = npts
     Q = np.zeros((ncells, nout), dtype=np.float64)
-    G = np.zeros_like(Q)
-    Lo = np.zeros_like(Q)
+    G = np.zeros_like(Q) if diagnostics else None
+    Lo = np.zeros_like(Q) if diagnostics else None
     if dirs is None:
         nd, dp, keep = -1, None, None
     else:
@@ -135,10 +147,11 @@ def collide(f: np.ndarray, d: int, N: int, Nbar: int, Ntilde: int, L: float = 8.
     for w in (wa, wb):
         if w is not None and w.size != box:
             raise ValueError(f"weight tables must have (2Ñ+1)^d = {box} entries")
-    rc = lib().dvm_oracle_collide_w(d, N, Nbar, Ntilde, float(L), fa.ctypes.data, ncells, npts, pp,
+    rc = lib().dvm_oracle_collide_w(d, N, Nbar, Ntilde, float(L), fa.ctypes.data, ncells, npts, pp, per_cell,
                                     nd, dp, None if wa is None else wa.ctypes.data,
-                                    None if wb is None else wb.ctypes.data, Q.ctypes.data, G.ctypes.data,
-                                    Lo.ctypes.data, int(nthreads))
+                                    None if wb is None else wb.ctypes.data, Q.ctypes.data,
+                                    None if G is None else G.ctypes.data,
+                                    None if Lo is None else Lo.ctypes.data, int(nthreads))
     if rc != 0:
         raise ValueError(f"dvm_oracle_collide failed with {rc}")
     del keep, pk, wa, wb
