@@ -222,6 +222,20 @@ DVM_API dvm_status_t dvm_set_path(dvm_plan_t plan, int path);
  *     N out of range; the plan keeps the built-in weights), DVM_E_NOMEM. */
 DVM_API dvm_status_t dvm_set_weights(dvm_plan_t plan, const double *a_box, const double *b_box);
 
+/* Tuning and timing switches of a plan (never read from the environment):
+ *   "max_groups" cap on concurrent cell groups of the persistent 3D kernels
+ *                (0 = every group that fits, the default)
+ *   "g3_cl"      frame-plane kernel CTAs per cell group at N = 32: 4, 8
+ *                (default) or 16
+ *   "verbose"    1 = print launch geometry on stderr
+ *   "timing_dbg" skip work inside the 3D N = 64 kernel for phase timing (bits:
+ *                1 phase B, 2 phase A, 4 line taps).  Q IS WRONG while nonzero;
+ *                for profiling experiments only.
+ * None of the others changes Q beyond fp64 summation order.  Errors:
+ * DVM_E_NULL, DVM_E_STATE (unknown key or out-of-range value; the plan is
+ * unchanged). */
+DVM_API dvm_status_t dvm_set_tuning(dvm_plan_t plan, const char *key, int value);
+
 /* Wait for all work issued on the plan's stream; reports asynchronous faults. */
 DVM_API dvm_status_t dvm_sync(dvm_plan_t plan);
 

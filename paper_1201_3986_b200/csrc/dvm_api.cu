@@ -216,8 +216,18 @@ dvm_status_t dvm_plan_info(dvm_plan_t P, dvm_plan_info_t *info)
     info->L = P->L;
     info->h = P->h;
     const Workspace &w = P->ws;
-    info->workspace_bytes = P->table_bytes + sizeof(double) * (w.slots * w.slot_elems * (w.part ? 2 : 1)) +
-                            sizeof(double) * 2 * w.stage_elems;
+    // every device buffer the plan holds: tables, evaluation workspaces, staging
+    const int64_t nd = nodes_of(P);
+    size_t bytes = P->table_bytes + P->g.bytes;
+    bytes += sizeof(double) * (size_t)w.slots * w.slot_elems * ((w.S ? 1 : 0) + (w.part ? 1 : 0));
+    bytes += sizeof(double) * 2 * w.stage_elems;
+    bytes += sizeof(double2) * (w.fft_z_elems + w.g3_f_elems + w.g3_t_elems + w.g3_q_elems + w.sp_z_elems +
+                                w.fg_fhat_elems);
+    bytes += sizeof(unsigned int) * w.g3_ctr_elems;
+    bytes += sizeof(double) * (w.p2_scr_elems + w.p2_part_elems);
+    bytes += sizeof(double) * (size_t)nd * ((w.qtmp ? 1 : 0) + (w.f1tmp ? 1 : 0));
+    bytes += sizeof(double) * (kMaxD + 2) * w.mom_rows;
+    info->workspace_bytes = bytes;
     info->launches = P->launches;
     return DVM_OK;
 }
@@ -546,6 +556,35 @@ dvm_status_t dvm_set_path(dvm_plan_t P, int path)
         return DVM_E_STATE;
     }
     P->path_mode = path;
+    return DVM_OK;
+}
+
+dvm_status_t dvm_set_tuning(dvm_plan_t P, const char *key, int value)
+{
+    if (!P || !key) {
+        set_error("NULL argument");
+        return DVM_E_NULL;
+    }
+    const std::string k(key);
+    auto bad = [&]() {
+        set_error("dvm_set_tuning: bad value for " + k);
+        return DVM_E_STATE;
+    };
+    if (k == "max_groups") {
+        if (value < 0) return bad();
+        P->tune.max_groups = value;
+    } else if (k == "g3_cl") {
+        if (value != 0 && value != 4 && value != 8 && value != 16) return bad();
+        P->tune.g3_cl = value;
+    } else if (k == "verbose") {
+        P->tune.verbose = value != 0;
+    } else if (k == "timing_dbg") {
+        if (value < 0 || value > 7) return bad();
+        P->tune.fg_dbg = value;
+    } else {
+        set_error("dvm_set_tuning: unknown key " + k);
+        return DVM_E_STATE;
+    }
     return DVM_OK;
 }
 

@@ -1,5 +1,5 @@
 // dvm_fgain3d.cu -- 3D gain G = Σ_e a_e S_e T_e by per-direction FFT
-// filtering (sm_100a, fp64; N = 64).
+// filtering (sm_100a, fp64; N = 64): k_fg2.
 //
 // The perp sums are the periodic convolution T_e = f ⊛ 1_{P_e}; their filter
 // is even, so its spectrum is real and two cells share one complex transform:
@@ -8,19 +8,18 @@
 // with (u, w) the basis of e^⊥ ∩ Z^3 the rows of P_e are given in
 // (the paper's spectral evaluation of the α'_p
 // factor; only the perp factor goes through Fourier space here, S_e stays a
-// line stencil).  A persistent cooperative kernel; a group of CL CTAs owns
-// one cell pair at a time and walks the directions:
-//   phase A (warps 0-7): CTA `rank` takes the planes ξ_x ≡ rank (mod CL):
+// line stencil).  A persistent cooperative kernel; a group of 16 CTAs owns
+// one cell pair at a time and walks the directions, warp-specialised:
+//   phase A (warps 0-7): CTA `rank` takes the planes ξ_x ≡ rank (mod 16):
 //     cp.async the plane of f̂ into shared memory, multiply by t̂_e, inverse
-//     2D FFT over (ξ_y, ξ_z) (64 = 8 × 8 four-step, one shared-memory
-//     exchange per axis), write the plane to the group's ring slot.
-//   group progress counters (per CTA, monotonic)
+//     2D FFT over (ξ_y, ξ_z) with 16 points per thread (details below), write
+//     the plane to the group's ring slot [ξ_x][y][z] in L2.
+//   group progress counters (per CTA, monotonic, acquire/release)
 //   phase B (warps 8-15): CTA `rank` owns the rows y ∈ [4 rank, 4 rank + 4):
 //     ring columns loaded straight into registers one batch ahead, inverse FFT
-//     along ξ_x of its 256 columns, then Q += a_e S_e T_e with
-//     S_e = Σ_{1<=|m|<=M_e} f(.+me) read as coalesced taps; Q lives in TMEM.
-//   The roles run separate loops so setmaxnreg can move registers from A (88)
-//   to B (168).
+//     along ξ_x (64 = 8 × 8, one shared-memory exchange), then Q += a_e S_e T_e
+//     with S_e = Σ_{1<=|m|<=M_e} f(.+me) read as coalesced taps; Q lives in TMEM.
+//   The roles run separate loops so setmaxnreg can move registers between them.
 // Loss and the layout conversions are shared with dvm_gain3d.cu.
 #include <math.h>
 #include <stdio.h>
@@ -39,21 +38,9 @@ using namespace g3;
 constexpr int FN = 64;           // grid points per axis (64 = 8 × 8)
 constexpr int FN2 = FN * FN;
 constexpr int64_t FNODES = (int64_t)FN * FN * FN;
-constexpr int FRS = FN + 1;      // padded row pitch of a plane in shared memory (double2)
-constexpr int FTP = FN + 1;      // padded row pitch of the T2D table (double)
-constexpr int FTR = FN / 2 + 1;  // rows of T2D kept in shared memory (the table is even: T(-p,-q) = T(p,q))
 constexpr int FMS = 32;          // tap table size (2 M_e <= 32)
-#ifndef FG_TAPUNROLL
-#define FG_TAPUNROLL 1  // 8 loads in flight per tap pair; unrolling further measured slower
-#endif
-constexpr int kTapUnroll = FG_TAPUNROLL;
-constexpr int kRegA = 88, kRegB = 168;
-#ifndef FG_TF_REGA
-#define FG_TF_REGA 96
-#endif
-constexpr int kRegATF = FG_TF_REGA, kRegBTF = 256 - FG_TF_REGA;  // TF: A holds 8 more TMEM words  // setmaxnreg split of the 128 x 512 register file (A + B <= 256)
-#ifndef FG_TAPLD
-#define FG_TAPLD ld2_nc_hint
+#ifndef FG2_REGA
+#define FG2_REGA 104  // k_fg2 setmaxnreg split: phase A, phase B gets 256 - FG2_REGA
 #endif
 
 struct FgArgs {
@@ -69,19 +56,9 @@ struct FgArgs {
     unsigned int *ctr;    // [groups][2][CL]
     uint32_t H;
     int slots;            // ring depth per group (phase A runs up to slots-1 steps ahead)
-    int dbg;              // timing experiments (DVM_FG_DEBUG): 1 skip phase-B work, 2 skip phase-A work,
+    int dbg;              // timing experiments (dvm_set_tuning "timing_dbg"; Q wrong): 1 skip phase-B work, 2 skip phase-A work,
                           // 4 skip the taps
 };
-
-template <bool TF>
-struct FgSmemT {
-    static constexpr size_t xb = sizeof(double2) * (TF ? 1 : 2) * FN * FRS;  // plane buffer(s)
-    static constexpr size_t t2 = (sizeof(double) * FTR * FTP + 127) / 128 * 128;  // T2D_e of the step, rows 0..N/2
-    static constexpr size_t rb = sizeof(double2) * 2 * FN * 32;   // phase-B x-FFT exchange, 2 batches
-    static constexpr size_t tw = sizeof(double2) * FN;            // W_64^k (inverse sign)
-    static constexpr size_t total = xb + t2 + rb + tw;
-};
-using FgSmem = FgSmemT<false>;
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b)
 {
@@ -118,11 +95,6 @@ __device__ __forceinline__ void idft8(double2 (&v)[8])
     v[7] = sub2(e3, o3);
 }
 
-// position of element z of a row after the in-row four-step (z = k2 + 8 k1 is
-// kept where its thread read it: 8 k2 + ((k1 + k2) & 7)); bank-conflict free
-// for lanes along rows and along columns
-__device__ __forceinline__ int zpos(int z) { return 8 * (z & 7) + (((z >> 3) + (z & 7)) & 7); }
-
 __device__ __forceinline__ void cp_async16_pol(void *smem_dst, const void *gsrc, uint64_t pol)
 {
     asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(
@@ -130,39 +102,6 @@ __device__ __forceinline__ void cp_async16_pol(void *smem_dst, const void *gsrc,
                  "l"(gsrc), "l"(pol)
                  : "memory");
 }
-__device__ __forceinline__ void cp_async8(void *smem_dst, const void *gsrc)
-{
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(smem_dst)),
-                 "l"(gsrc)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
-
-// 32 columns of this thread's TMEM lane (8 double2)
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32])
-{
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-        "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32])
-{
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-        "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
-        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
-        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
-        "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
-        "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
-        : "memory");
-}
-
 // progress counters of a group of CL CTAs (role_wait of dvm_g3common.h for CL <= 32)
 template <int CL>
 __device__ __forceinline__ void group_wait(const unsigned int *ctrs, unsigned int target, int t, int id)
@@ -186,23 +125,77 @@ __device__ __forceinline__ void group_wait(const unsigned int *ctrs, unsigned in
     role_sync(id);
 }
 
-// TF: f̂ of the group's cell pair resident in TMEM (groups of 32 CTAs: each CTA's 2
-// planes are 128 KB = TMEM columns 256-511; Q takes columns 0-255), no plane loads
-template <int CL, bool TF>
-__global__ void __launch_bounds__(2 * kRoleT, 1) k_fgain3d(FgArgs A)
+// ============================================================================
+// Phase A of k_fg2: 16 points per thread, 64 = 4 × 16 in both in-plane passes
+// (radix-4 over the high index in registers, one warp-private 16 × 16
+// transpose, a 16-point DFT; one CTA-wide exchange between the two axes), so
+// a plane costs 3 role barriers.  Plane ξ_x = g, thread t = (yl, zl), zl = t & 15,
+// yl = t >> 4, holds f̂(g, ξ_y = yl + 16 b, ξ_z = zl + 16 a), a, b < 4:
+//   z: radix-4 over a, × ω^{zl kp1}; y: radix-4 over b, × ω^{yl kq1}    (ω = e^{2πi/64})
+//   warp-private transpose: thread (yl, c = kp1 + 4 kq1) gets the 16 zl
+//   16-point DFT over zl → z = kp1 + 4 kp2
+//   CTA exchange: thread (z, kq1) gets the 16 yl;  16-point DFT → y = kq1 + 4 kq2
+//   ring slot [ξ_x][y][z] (coalesced along z)
+// Phase B: thread (k2 = warp, z = lane + 32 (b & 1)) of batch b (row
+// y = 4 rank + b / 2) holds H(ξ_x = k2 + 8 n2, y, z), n2 < 8: DFT-8,
+// twiddle, one shared-memory exchange across the 8 warps, DFT-8 → x = k2 + 8 k1.
+// Lanes run along z, so every ring load and every tap load of a warp covers
+// 512 contiguous bytes.
+// ============================================================================
+constexpr int kRegA2 = FG2_REGA, kRegB2 = 256 - FG2_REGA;
+constexpr int F2Q = FN2 / 4 + 4;  // CTA-exchange pitch of one kq1 quarter [16 yl][64 z] (+4: conflict-free writes)
+
+struct Fg2Smem {
+    static constexpr size_t st = sizeof(double2) * FN2;                        // f̂ plane staging / ex1 scratch
+    static constexpr size_t ex = sizeof(double2) * (3 * F2Q + FN2 / 4);        // CTA exchange [kq1][yl][z]
+    static constexpr size_t t2 = sizeof(double) * FN2;                         // T2D_e, full 64 × 64
+    static constexpr size_t tw = sizeof(double2) * FN;                         // ω^k
+    static constexpr size_t rb = sizeof(double2) * 2 * FN * 32;                // phase-B exchange, 2 batches
+    static constexpr size_t total = st + ex + t2 + tw + rb;
+};
+
+// inverse 16-point DFT, natural order in and out: n = n1 + 4 n2, k = k1 + 4 k2
+__device__ __forceinline__ void idft16(double2 (&v)[16])
 {
-    static_assert(!TF || CL == 32, "TMEM-resident f̂ needs 2 planes per CTA");
-    using Sm = FgSmemT<TF>;
+    constexpr double c1 = 0.92387953251128675613, s1 = 0.38268343236508977173, c2 = 0.70710678118654752440;
+#pragma unroll
+    for (int n1 = 0; n1 < 4; ++n1) idft4(v[n1], v[n1 + 4], v[n1 + 8], v[n1 + 12]);  // v[n1 + 4 k1]
+    // × ω16^{n1 k1}
+    auto rot = [](double2 x, double c, double s) { return make_double2(x.x * c - x.y * s, x.x * s + x.y * c); };
+    v[5] = rot(v[5], c1, s1);                                            // n1 = 1, k1 = 1: ω^1
+    v[9] = make_double2(c2 * (v[9].x - v[9].y), c2 * (v[9].x + v[9].y));  // n1 = 1, k1 = 2: ω^2
+    v[13] = rot(v[13], s1, c1);                                          // n1 = 1, k1 = 3: ω^3
+    v[6] = make_double2(c2 * (v[6].x - v[6].y), c2 * (v[6].x + v[6].y));  // n1 = 2, k1 = 1: ω^2
+    v[10] = make_double2(-v[10].y, v[10].x);                             // n1 = 2, k1 = 2: ω^4 = i
+    v[14] = make_double2(-c2 * (v[14].x + v[14].y), c2 * (v[14].x - v[14].y));  // n1 = 2, k1 = 3: ω^6
+    v[7] = rot(v[7], s1, c1);                                            // n1 = 3, k1 = 1: ω^3
+    v[11] = make_double2(-c2 * (v[11].x + v[11].y), c2 * (v[11].x - v[11].y));  // n1 = 3, k1 = 2: ω^6
+    v[15] = rot(v[15], -c1, -s1);                                        // n1 = 3, k1 = 3: ω^9
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) idft4(v[4 * k1], v[4 * k1 + 1], v[4 * k1 + 2], v[4 * k1 + 3]);  // v[4 k1 + k2]
+    double2 o[16];
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1)
+#pragma unroll
+        for (int k2 = 0; k2 < 4; ++k2) o[k1 + 4 * k2] = v[4 * k1 + k2];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = o[k];
+}
+
+template <int CL>
+__global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
+{
     constexpr int FPL = FN / CL;  // ξ_x planes per CTA per direction
-    constexpr int FRY = FN / CL;  // phase-B rows y per CTA
-    constexpr int NBAT = 2 * FRY; // phase-B batches (one row y, 32 columns z)
+    constexpr int FRY = FN / CL;  // phase-B rows y per CTA (one batch each)
+    static_assert(FRY == 4, "TMEM holds 4 rows of node pairs per CTA");
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    double2 *xb = reinterpret_cast<double2 *>(smem_raw);                            // [2][FN][FRS]
-    double *t2 = reinterpret_cast<double *>(smem_raw + Sm::xb);                      // [FTR][FTP]
-    double2 *rb = reinterpret_cast<double2 *>(smem_raw + Sm::xb + Sm::t2);           // [2][FN][32]
-    double2 *tw = rb + 2 * FN * 32;                                                  // [FN]
-    __shared__ uint32_t soff[FMS];
-    __shared__ int smB[4];
+    double2 *stg = reinterpret_cast<double2 *>(smem_raw);                                 // [FN][FN]
+    double2 *ex = reinterpret_cast<double2 *>(smem_raw + Fg2Smem::st);                    // [4][F2Q]
+    double *t2 = reinterpret_cast<double *>(smem_raw + Fg2Smem::st + Fg2Smem::ex);        // [FN][FN]
+    double2 *tw = reinterpret_cast<double2 *>(smem_raw + Fg2Smem::st + Fg2Smem::ex + Fg2Smem::t2);  // [FN]
+    double2 *rb = tw + FN;  // phase-B x-FFT exchange [2][FN][32]
+    __shared__ uint32_t soff[2][FMS];
+    __shared__ uint32_t s_tmem;
 
     const bool roleA = threadIdx.x < kRoleT;
     const int t = threadIdx.x & (kRoleT - 1);
@@ -222,7 +215,6 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fgain3d(FgArgs A)
         sincospi(2.0 * threadIdx.x / FN, &s, &c);
         tw[threadIdx.x] = make_double2(c, s);
     }
-    __shared__ uint32_t s_tmem;
     if (!roleA && warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"l"(
                          (uint64_t)__cvta_generic_to_shared(&s_tmem))
@@ -232,227 +224,145 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fgain3d(FgArgs A)
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    // B: Q accumulators (64 or 32 node pairs per thread); A (TF): the f̂ planes
-    constexpr uint32_t QCOLS = TF ? 128 : 256;
-    const uint32_t tm_lane = s_tmem + ((uint32_t)(32 * (warp & 3)) << 16);
-    const uint32_t tm_base = roleA ? (TF ? tm_lane + 256u + 128u * (warp >> 2) : 0u) : tm_lane + QCOLS * (warp >> 2);
 
-    // phase A loads: T2D_e (8-byte pieces into padded rows) and planes of f̂
     auto load_t2d = [&](int di) {
-        const double *src = A.t2d + (int64_t)di * FN2;
-        for (int i = t; i < FTR * FN; i += kRoleT) cp_async8(t2 + (i >> 6) * FTP + (i & 63), src + i);
-        cp_async_commit();
+        const double2 *src = reinterpret_cast<const double2 *>(A.t2d + (int64_t)di * FN2);
+        for (int i = t; i < FN2 / 2; i += kRoleT) cp_async16_pol(t2 + 2 * i, src + i, l2_keep());
     };
-    auto load_plane = [&](const double2 *fh, int g, double2 *dst) {
+    auto load_plane = [&](const double2 *fh, int g) {
         const double2 *src = fh + (int64_t)g * FN2;
-        // f̂ streams (evict first): L2 is kept for f (taps) and the ring
-        const uint64_t pol = (A.dbg & 32) ? l2_keep() : l2_drop();
-        for (int i = t; i < FN2; i += kRoleT) cp_async16_pol(dst + (i >> 6) * FRS + (i & 63), src + i, pol);
-        cp_async_commit();
+        const uint64_t pol = l2_drop();  // f̂ streams; L2 is kept for f (taps) and the ring
+        for (int i = t; i < FN2; i += kRoleT) cp_async16_pol(stg + i, src + i, pol);
     };
-    // TF: the planes ξ_x = rank + CL kp of a pair into this thread's TMEM columns,
-    // [kp][h][n2] x double2: exactly the row-pass inputs of thread (n1 = warp, r = lane + 32 h)
-    auto load_fhat_tmem = [&](const double2 *fh) {
-#pragma unroll 1
-        for (int kp = 0; kp < 2; ++kp)
-#pragma unroll 1
-            for (int h = 0; h < 2; ++h) {
-                uint32_t r[32];
-                const double2 *src = fh + (int64_t)(rank + CL * kp) * FN2 + (lane + 32 * h) * FN + warp;
-#pragma unroll
-                for (int n2 = 0; n2 < 8; ++n2) {
-                    const double2 x = src[8 * n2];
-                    r[4 * n2 + 0] = __double2loint(x.x);
-                    r[4 * n2 + 1] = __double2hiint(x.x);
-                    r[4 * n2 + 2] = __double2loint(x.y);
-                    r[4 * n2 + 3] = __double2hiint(x.y);
-                }
-                __syncwarp();
-                tmem_st32(tm_base + 64u * kp + 32u * h, r);
-            }
-        tmem_wait_st();
-    };
-    if (roleA && grp < items && !(A.dbg & 2)) {
-        if constexpr (!TF) load_plane(A.fhat + (grp / A.nchunks) * FNODES, rank, xb);
-        load_t2d((int)((int64_t)A.nloc * (grp % A.nchunks) / A.nchunks));
-    }
 
     if (roleA) {
-        // phase A fits in 88 registers; phase B takes the rest (register prefetch of the ring)
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(TF ? kRegATF : kRegA));
-    for (int64_t item = grp; item < items; item += ngroups) {
-        const int64_t pair = item / A.nchunks;
-        const int chunk = (int)(item % A.nchunks);
-        const int d0 = (int)((int64_t)A.nloc * chunk / A.nchunks);
-        const int d1 = (int)((int64_t)A.nloc * (chunk + 1) / A.nchunks);
-        const double2 *__restrict__ fh = A.fhat + pair * FNODES;
-        if constexpr (TF) {
-            if (!(A.dbg & 2)) load_fhat_tmem(fh);
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegA2));
+        const int zl = t & 15, yl = t >> 4;
+        // ex1 scratch of this half-warp: the 4 staging rows it read, yl + 16 b
+        double2 *x1w = stg + yl * FN;
+        const int c_me = zl;  // after the transpose: c = kp1 + 4 kq1
+        const int sw = c_me & 7;
+        const int zr = t & 63, kq1r = t >> 6;  // CTA exchange reader: (z, kq1)
+        if (grp < items && !(A.dbg & 2)) {
+            load_plane(A.fhat + (grp / A.nchunks) * FNODES, rank);
+            load_t2d((int)((int64_t)A.nloc * (grp % A.nchunks) / A.nchunks));
+            cp_async_commit();
         }
-
-        for (int di = d0; di < d1; ++di, ++stepi) {
-            double2 *Tb = A.ring + ((int64_t)grp * A.slots + (stepi % A.slots)) * FNODES;
-            // the group's next step (direction, cell pair), -1 at the end
-            int ndi = -1;
-            const double2 *fh_next = fh;
-            if (di + 1 < d1) {
-                ndi = di + 1;
-            } else if (item + ngroups < items) {
-                ndi = (int)((int64_t)A.nloc * ((item + ngroups) % A.nchunks) / A.nchunks);
-                fh_next = A.fhat + ((item + ngroups) / A.nchunks) * FNODES;
-            }
-            {
-                // ============================================ phase A: planes of IFFT_yz(f̂ t̂_e)
-                // (T2D_e and the first plane are in flight since the previous step)
+        for (int64_t item = grp; item < items; item += ngroups) {
+            const int64_t pair = item / A.nchunks;
+            const int chunk = (int)(item % A.nchunks);
+            const int d0 = (int)((int64_t)A.nloc * chunk / A.nchunks);
+            const int d1 = (int)((int64_t)A.nloc * (chunk + 1) / A.nchunks);
+            const double2 *__restrict__ fh = A.fhat + pair * FNODES;
+            for (int di = d0; di < d1; ++di, ++stepi) {
+                double2 *Tb = A.ring + ((int64_t)grp * A.slots + (stepi % A.slots)) * FNODES;
+                int ndi = -1;
+                const double2 *fh_next = fh;
+                if (di + 1 < d1) {
+                    ndi = di + 1;
+                } else if (item + ngroups < items) {
+                    ndi = (int)((int64_t)A.nloc * ((item + ngroups) % A.nchunks) / A.nchunks);
+                    fh_next = A.fhat + ((item + ngroups) / A.nchunks) * FNODES;
+                }
                 if (stepi >= (unsigned)A.slots) group_wait<CL>(cB, stepi - A.slots + 1, t, bar);
                 const int4 ru = A.rec[(int64_t)di * 3 + 1], rw = A.rec[(int64_t)di * 3 + 2];
                 const uint64_t keep = l2_keep();
-                int cur = 0;
 #pragma unroll 1
                 for (int kp = 0; kp < ((A.dbg & 2) ? 0 : FPL); ++kp) {
                     const int g = rank + kp * CL;
                     const bool lastp = kp + 1 == FPL;
-                    if constexpr (TF) {
-                        if (kp == 0) {
-                            cp_async_wait_all();  // T2D_e of this step
-                            role_sync(bar);
-                        }
-                    } else {
-                        if (!lastp) {
-                            load_plane(fh, g + CL, xb + (cur ^ 1) * FN * FRS);
-                            cp_async_wait1();
-                        } else {
-                            cp_async_wait_all();
-                        }
-                        role_sync(bar);
-                        // the last plane: the next step's first plane goes into the other buffer
-                        if (lastp && ndi >= 0) load_plane(fh_next, rank, xb + (cur ^ 1) * FN * FRS);
-                    }
-                    double2 *X = xb + (TF ? 0 : cur) * FN * FRS;
-                    double2 v[8];
-                    // --- rows: t̂ multiply, inverse FFT along ξ_z (four-step 8 × 8)
-#pragma unroll 1
-                    for (int h = 0; h < 2; ++h) {
-                        const int r = lane + 32 * h;  // ξ_y
-                        {
-                            const int n1 = warp;
-                            int pu = (ru.x * g + ru.y * r + ru.z * n1) & (FN - 1);
-                            int pw = (rw.x * g + rw.y * r + rw.z * n1) & (FN - 1);
-                            const int du = (8 * ru.z) & (FN - 1), dw = (8 * rw.z) & (FN - 1);
-                            uint32_t fr[TF ? 32 : 1];
-                            if constexpr (TF) {
-                                __syncwarp();
-                                tmem_ld32(tm_base + 64u * kp + 32u * h, fr);
+                    cp_async_wait_all();
+                    role_sync(bar);  // [1] the plane (and at kp = 0 T2D_e) is in shared memory
+                    double2 v[16];
+                    {
+                        // stage 1: f̂ t̂_e, radix-4 over ξ_z high and ξ_y high
+                        const int pu0 = ru.x * g + ru.y * yl + ru.z * zl, pw0 = rw.x * g + rw.y * yl + rw.z * zl;
+                        const int dua = 16 * ru.z, dub = 16 * ru.y, dwa = 16 * rw.z, dwb = 16 * rw.y;
+#pragma unroll
+                        for (int b = 0; b < 4; ++b)
+#pragma unroll
+                            for (int a = 0; a < 4; ++a) {
+                                const int pu = (pu0 + a * dua + b * dub) & (FN - 1);
+                                const int pw = (pw0 + a * dwa + b * dwb) & (FN - 1);
+                                const double tv = t2[pu * FN + pw];
+                                const double2 x = stg[(yl + 16 * b) * FN + zl + 16 * a];
+                                v[a + 4 * b] = make_double2(x.x * tv, x.y * tv);
                             }
 #pragma unroll
-                            for (int n2 = 0; n2 < 8; ++n2) {
-                                // rows p > N/2 from the even symmetry T(p, q) = T(N - p, N - q)
-                                const bool up = pu > FN / 2;
-                                const int tp = up ? FN - pu : pu, tq = up ? (FN - pw) & (FN - 1) : pw;
-                                const double tv = t2[tp * FTP + tq];
-                                double2 x;
-                                if constexpr (TF)
-                                    x = make_double2(__hiloint2double(fr[4 * n2 + 1], fr[4 * n2]),
-                                                     __hiloint2double(fr[4 * n2 + 3], fr[4 * n2 + 2]));
-                                else
-                                    x = X[r * FRS + n1 + 8 * n2];
-                                v[n2] = make_double2(x.x * tv, x.y * tv);
-                                pu = (pu + du) & (FN - 1);
-                                pw = (pw + dw) & (FN - 1);
-                            }
-                            idft8(v);
+                        for (int b = 0; b < 4; ++b) idft4(v[4 * b], v[4 * b + 1], v[4 * b + 2], v[4 * b + 3]);
 #pragma unroll
-                            for (int k2 = 1; k2 < 8; ++k2) v[k2] = cmul(v[k2], tw[(n1 * k2) & (FN - 1)]);
-                            if constexpr (!TF) role_sync(bar);  // other warps still read the staged plane
+                        for (int b = 0; b < 4; ++b)
 #pragma unroll
-                            for (int k2 = 0; k2 < 8; ++k2) X[r * FRS + 8 * k2 + ((n1 + k2) & 7)] = v[k2];
-                        }
-                        role_sync(bar);
-                        {
-                            const int k2 = warp;
+                            for (int k = 1; k < 4; ++k) v[k + 4 * b] = cmul(v[k + 4 * b], tw[(zl * k) & (FN - 1)]);  // ω^{zl kp1}
 #pragma unroll
-                            for (int n1 = 0; n1 < 8; ++n1) v[n1] = X[r * FRS + 8 * k2 + ((n1 + k2) & 7)];
-                            idft8(v);
+                        for (int k = 0; k < 4; ++k) idft4(v[k], v[k + 4], v[k + 8], v[k + 12]);
 #pragma unroll
-                            for (int k1 = 0; k1 < 8; ++k1) X[r * FRS + 8 * k2 + ((k1 + k2) & 7)] = v[k1];
-                        }
+                        for (int q = 1; q < 4; ++q)
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) v[k + 4 * q] = cmul(v[k + 4 * q], tw[(yl * q) & (FN - 1)]);  // ω^{yl kq1}
                     }
-                    role_sync(bar);
-                    if (lastp && ndi >= 0) load_t2d(ndi);  // t2 is free: the next direction's table
-                    // --- columns: inverse FFT along ξ_y, plane -> ring slot [ξ_x][y][z]
-#pragma unroll 1
-                    for (int h = 0; h < 2; ++h) {
-                        const int z = lane + 32 * h;
-                        const int pz = zpos(z);
-                        {
-                            const int n1 = warp;
+                    // warp-private 16 × 16 transpose in the rows this half-warp read:
+                    // entry (c, zl) at c·16 + (zl ^ (c & 7)) of the 256-entry block
+                    __syncwarp();
 #pragma unroll
-                            for (int n2 = 0; n2 < 8; ++n2) v[n2] = X[(n1 + 8 * n2) * FRS + pz];
-                            idft8(v);
+                    for (int c = 0; c < 16; ++c)
+                        x1w[(c >> 2) * 16 * FN + 16 * (c & 3) + (zl ^ (c & 7))] = v[c];
+                    __syncwarp();
 #pragma unroll
-                            for (int k2 = 1; k2 < 8; ++k2) v[k2] = cmul(v[k2], tw[(n1 * k2) & (FN - 1)]);
-                            role_sync(bar);
-#pragma unroll
-                            for (int k2 = 0; k2 < 8; ++k2) X[(8 * k2 + ((n1 + k2) & 7)) * FRS + pz] = v[k2];
-                        }
-                        role_sync(bar);
-                        {
-                            const int k2 = warp;
-#pragma unroll
-                            for (int n1 = 0; n1 < 8; ++n1) v[n1] = X[(8 * k2 + ((n1 + k2) & 7)) * FRS + pz];
-                            idft8(v);
-                            double2 *dst = Tb + (int64_t)g * FN2 + z;
-#pragma unroll
-                            for (int k1 = 0; k1 < 8; ++k1) st2_hint(dst + (k2 + 8 * k1) * FN, v[k1], keep);
-                        }
+                    for (int n = 0; n < 16; ++n)
+                        v[n] = x1w[(c_me >> 2) * 16 * FN + 16 * (c_me & 3) + (n ^ sw)];
+                    idft16(v);  // z = kp1 + 4 kp2: v[kp2], kp1 = c_me & 3
+                    role_sync(bar);  // [2] staging and the exchange buffer are free
+                    if (!lastp) {
+                        load_plane(fh, g + CL);
+                    } else if (ndi >= 0) {
+                        load_plane(fh_next, rank);
+                        load_t2d(ndi);
                     }
-                    role_sync(bar);  // X is free for the next prefetch
-                    cur ^= 1;
+                    cp_async_commit();
+                    {
+                        const int kp1 = c_me & 3, kq1 = c_me >> 2;
+                        double2 *dst = ex + kq1 * F2Q + yl * FN + kp1;
+#pragma unroll
+                        for (int k = 0; k < 16; ++k) dst[4 * k] = v[k];
+                    }
+                    role_sync(bar);  // [3]
+                    {
+                        const double2 *src = ex + kq1r * F2Q + zr;
+#pragma unroll
+                        for (int n = 0; n < 16; ++n) v[n] = src[n * FN];
+                    }
+                    idft16(v);  // y = kq1r + 4 kq2: v[kq2]
+                    double2 *dst = Tb + (int64_t)g * FN2 + zr;
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) st2_hint(dst + (kq1r + 4 * k) * FN, v[k], keep);
                 }
                 role_signal(cA + rank, stepi + 1, leader, bar);
             }
         }
-    }
+        cp_async_wait_all();
     } else {
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(TF ? kRegBTF : kRegB));
-    for (int64_t item = grp; item < items; item += ngroups) {
-        const int64_t pair = item / A.nchunks;
-        const int chunk = (int)(item % A.nchunks);
-        const int d0 = (int)((int64_t)A.nloc * chunk / A.nchunks);
-        const int d1 = (int)((int64_t)A.nloc * (chunk + 1) / A.nchunks);
-        const double2 *__restrict__ fh = A.fhat + pair * FNODES;
-        const double2 *__restrict__ fc = A.f + pair * FNODES;
-        double2 *Qc = A.Q + ((int64_t)chunk * A.npairs + pair) * FNODES;
-
-        for (int di = d0; di < d1; ++di, ++stepi) {
-            double2 *Tb = A.ring + ((int64_t)grp * A.slots + (stepi % A.slots)) * FNODES;
-            // the group's next step (direction, cell pair), -1 at the end
-            int ndi = -1;
-            const double2 *fh_next = fh;
-            if (di + 1 < d1) {
-                ndi = di + 1;
-            } else if (item + ngroups < items) {
-                ndi = (int)((int64_t)A.nloc * ((item + ngroups) % A.nchunks) / A.nchunks);
-                fh_next = A.fhat + ((item + ngroups) / A.nchunks) * FNODES;
-            }
-            {
-                // ============================================ phase B: IFFT_x, Q += a_e S_e T_e
-                if (t == 0) {
-                    const int4 re = A.rec[(int64_t)di * 3];
-                    smB[0] = re.x;
-                    smB[1] = re.y;
-                    smB[2] = re.z;
-                    smB[3] = re.w;
-                }
-                group_wait<CL>(cA, stepi + 1, t, bar);
-                const int M = smB[3];
-                if (t < 2 * M) {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegB2));
+        const uint32_t tm_base = s_tmem + ((uint32_t)(32 * (warp & 3)) << 16) + 256u * (uint32_t)(warp >> 2);
+        for (int64_t item = grp; item < items; item += ngroups) {
+            const int64_t pair = item / A.nchunks;
+            const int chunk = (int)(item % A.nchunks);
+            const int d0 = (int)((int64_t)A.nloc * chunk / A.nchunks);
+            const int d1 = (int)((int64_t)A.nloc * (chunk + 1) / A.nchunks);
+            const double2 *__restrict__ fc = A.f + pair * FNODES;
+            double2 *Qc = A.Q + ((int64_t)chunk * A.npairs + pair) * FNODES;
+            for (int di = d0; di < d1; ++di, ++stepi) {
+                const double2 *Tb = A.ring + ((int64_t)grp * A.slots + (stepi % A.slots)) * FNODES;
+                const int4 re = A.rec[(int64_t)di * 3];
+                const int M2 = 2 * re.w;
+                uint32_t *so = soff[stepi & 1];
+                if (t < M2) {
                     const int m = t / 2 + 1, sg = (t & 1) ? -1 : 1;
-                    soff[t] = pk<FN>(sg * m * smB[0], sg * m * smB[1], sg * m * smB[2]);
+                    so[t] = pk<FN>(sg * m * re.x, sg * m * re.y, sg * m * re.z);
                 }
-                const bool first = di == d0, last = di == d1 - 1;
                 const double aw = A.aw[di];
-                const int M2 = 2 * M;
+                const bool first = di == d0, last = di == d1 - 1;
+                group_wait<CL>(cA, stepi + 1, t, bar);  // the ring slot is complete (and soff visible)
                 const uint64_t keep = l2_keep(), drop = l2_drop();
                 // ring columns straight into registers, one batch ahead (coalesced 512 B per warp row)
                 double2 pre[8];
@@ -463,7 +373,7 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fgain3d(FgArgs A)
                 };
                 if (!(A.dbg & 1)) fetch(0);
 #pragma unroll 1
-                for (int b = 0; b < ((A.dbg & 1) ? 0 : NBAT); ++b) {
+                for (int b = 0; b < ((A.dbg & 1) ? 0 : (2 * FRY)); ++b) {
                     const int y = FRY * rank + (b >> 1), z = 32 * (b & 1) + lane;
                     double2 v[8];
                     // buffer of pass-1 outputs: batch b - 2 used it, every thread is past b - 1's barrier
@@ -472,7 +382,7 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fgain3d(FgArgs A)
                         const int n1 = warp;
 #pragma unroll
                         for (int n2 = 0; n2 < 8; ++n2) v[n2] = pre[n2];
-                        if (b + 1 < NBAT) fetch(b + 1);
+                        if (b + 1 < (2 * FRY)) fetch(b + 1);
                         idft8(v);
 #pragma unroll
                         for (int k2 = 1; k2 < 8; ++k2) v[k2] = cmul(v[k2], tw[(n1 * k2) & (FN - 1)]);
@@ -500,17 +410,17 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fgain3d(FgArgs A)
                             S[q] = make_double2(0.0, 0.0);
                         }
                         // taps ±m e in pairs (M2 is even): 8 independent loads per iteration
-#pragma unroll kTapUnroll
+#pragma unroll 1  // 8 loads in flight per tap pair; unrolling further measured slower
                         for (int k = 0; k < ((A.dbg & 4) ? 0 : M2); k += 2) {
-                            const uint32_t o0 = soff[k], o1 = soff[k + 1];
+                            const uint32_t o0 = so[k], o1 = so[k + 1];
                             double2 a[4], c[4];
                             // the 4 nodes differ only in x (the top field, 8 q apart): one carry-less
                             // add per tap, then plain adds modulo N^3 for the other nodes
                             const uint32_t b0 = swar_add(n[0], o0, H2), b1 = swar_add(n[0], o1, H2);
 #pragma unroll
                             for (int q = 0; q < 4; ++q) {
-                                a[q] = FG_TAPLD(fc + ((b0 + (uint32_t)q * 8u * FN2) & (uint32_t)(FNODES - 1)), keep);
-                                c[q] = FG_TAPLD(fc + ((b1 + (uint32_t)q * 8u * FN2) & (uint32_t)(FNODES - 1)), keep);
+                                a[q] = ld2_nc_hint(fc + ((b0 + (uint32_t)q * 8u * FN2) & (uint32_t)(FNODES - 1)), keep);
+                                c[q] = ld2_nc_hint(fc + ((b1 + (uint32_t)q * 8u * FN2) & (uint32_t)(FNODES - 1)), keep);
                             }
 #pragma unroll
                             for (int q = 0; q < 4; ++q) S[q] = add2(S[q], add2(a[q], c[q]));
@@ -553,7 +463,6 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fgain3d(FgArgs A)
                 role_signal(cB + rank, stepi + 1, leader, bar);
             }
         }
-    }
     }
     if (!roleA) {
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -634,15 +543,9 @@ dvm_status_t collide_fgain3d(dvm_plan_s *P, const double *f, int64_t f_stride, d
         if (P->h_M[di] > FMS / 2) return DVM_OK;
     dvm_status_t st;
     if ((st = build_fg_tables(P))) return st;
-    // DVM_FG_TMEM=1: groups of 32 CTAs with f̂ resident in TMEM (k_fgain3d<32, true>)
-    const bool tf = getenv("DVM_FG_TMEM") && atoi(getenv("DVM_FG_TMEM")) != 0;
-    const int CL = tf ? 32 : (getenv("DVM_FG_CL") ? atoi(getenv("DVM_FG_CL")) : 16);
-    if (CL != 16 && CL != 32) {
-        set_error("DVM_FG_CL must be 16 or 32");
-        return DVM_E_UNSUPPORTED;
-    }
-    auto kern = tf ? k_fgain3d<32, true> : (CL == 16 ? k_fgain3d<16, false> : k_fgain3d<32, false>);
-    const size_t smem = tf ? FgSmemT<true>::total : FgSmemT<false>::total;
+    constexpr int CL = 16;
+    auto kern = k_fg2<CL>;
+    const size_t smem = Fg2Smem::total;
     DVM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int dev = 0, sms = 0, per_sm = 0, coop = 0;
     DVM_CUDA(cudaGetDevice(&dev));
@@ -650,8 +553,11 @@ dvm_status_t collide_fgain3d(dvm_plan_s *P, const double *f, int64_t f_stride, d
     DVM_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
     DVM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 2 * kRoleT, smem));
     if (!coop || per_sm < 1) return DVM_OK;  // the caller evaluates another path
+    // every CTA allocates all 512 TMEM columns: one CTA per SM (a second resident
+    // CTA would block in tcgen05.alloc while its group waits for it)
+    per_sm = 1;
     int max_groups = (sms * per_sm) / CL;
-    if (getenv("DVM_G3_GROUPS")) max_groups = std::max(1, std::min(max_groups, atoi(getenv("DVM_G3_GROUPS"))));
+    if (P->tune.max_groups) max_groups = std::max(1, std::min(max_groups, P->tune.max_groups));
     const int nloc = (int)P->local.size();
     const int64_t npairs = (ncells + 1) / 2;
     // direction chunks per pair: the persistent groups take (pair, chunk) items round-robin;
@@ -671,7 +577,7 @@ dvm_status_t collide_fgain3d(dvm_plan_s *P, const double *f, int64_t f_stride, d
     if ((st = grow(&w.g3_f, &w.g3_f_elems, (size_t)(npairs * FNODES), P->stream))) return st;
     if ((st = grow(&w.fg_fhat, &w.fg_fhat_elems, (size_t)(npairs * FNODES), P->stream))) return st;
     if ((st = grow(&w.g3_q, &w.g3_q_elems, (size_t)(nchunks * npairs * FNODES), P->stream))) return st;
-    const int slots = getenv("DVM_FG_SLOTS") ? std::max(2, std::min(4, atoi(getenv("DVM_FG_SLOTS")))) : 2;
+    const int slots = 2;  // ring depth: phase A runs at most one step ahead of phase B
     if ((st = grow(&w.g3_t, &w.g3_t_elems, (size_t)ngroups * slots * FNODES, P->stream))) return st;
     if ((st = grow(&w.g3_ctr, &w.g3_ctr_elems, (size_t)ngroups * 2 * CL, P->stream))) return st;
     if ((st = interleave_pairs(P, f, f_stride, ncells, FNODES, w.g3_f))) return st;
@@ -695,8 +601,8 @@ dvm_status_t collide_fgain3d(dvm_plan_s *P, const double *f, int64_t f_stride, d
     a.ctr = w.g3_ctr;
     a.H = P->pk.H;
     a.slots = slots;
-    a.dbg = getenv("DVM_FG_DEBUG") ? atoi(getenv("DVM_FG_DEBUG")) : 0;
-    if (getenv("DVM_VERBOSE"))
+    a.dbg = P->tune.fg_dbg;
+    if (P->tune.verbose)
         fprintf(stderr, "[dvm] fgain3d: %d groups x %d CTAs, %d chunks, smem %zu\n", ngroups, CL, nchunks, smem);
     {
         void *args[] = {&a};

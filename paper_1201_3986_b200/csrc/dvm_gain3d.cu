@@ -52,7 +52,6 @@ struct GainArgs {
     double2 *Tbuf;      // [groups][kSlots][nodes]
     unsigned int *ctr;  // [groups][2][kCL]: steps completed by each CTA's phase A / phase B
     uint32_t H;
-    int dbg;
 };
 
 constexpr int kSlots = 2;   // T ring depth per group (phase A may run kSlots-1 steps ahead)
@@ -214,9 +213,7 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_gain3d(GainArgs A)
                     const int g = rank + kp * CL;
                     cp_async_wait_all();
                     role_sync(bar);  // plane g is in rawb[cur] (and the next record is visible)
-                    if (A.dbg & 8) {
-                        // timing experiment: no gather (T on stale data)
-                    } else if (kp + 1 < NPL)
+                    if (kp + 1 < NPL)
                         gather_plane<N>(fc, rawb + (cur ^ 1) * Gm::PL, g + CL, smA + 3, t, H2);
                     else if (ndi >= 0)
                         gather_plane<N>(fnext, rawb + (cur ^ 1) * Gm::PL, rank,
@@ -226,7 +223,7 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_gain3d(GainArgs A)
                     // 16-column quarters: lanes 8q + i take row 8w + i, quarter q, so each
                     // quarter-warp reads 8 consecutive padded rows (conflict free); the
                     // quarter totals are combined with shuffles across lanes i, i+8, ...
-                    if (!(A.dbg & 16)) {
+                    {
                         constexpr int QN = 32 / 8;          // quarters per row (lanes per row)
                         constexpr int QL = N / QN;          // columns per quarter
                         constexpr int RPWARP = 8;           // rows per warp
@@ -266,7 +263,7 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_gain3d(GainArgs A)
                     role_sync(bar);
                     // A3: T by the sliding program (thread = column, β segment),
                     // stored straight from registers (16 bytes per node)
-                    if (!(A.dbg & 4)) {
+                    {
                         const int al = tal;
                         uint32_t x = pk<N>(g * z0 + al * u0 + tbe * w0, g * z1 + al * u1 + tbe * w1,
                                            g * z2 + al * u2 + tbe * w2);
@@ -353,7 +350,7 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_gain3d(GainArgs A)
                     soff[t] = pk<N>(sg * m * smB[0], sg * m * smB[1], sg * m * smB[2]);
                 }
                 role_sync(bar);
-                if (!(A.dbg & 2)) {
+                {
                     // thread-owned nodes n0 + t + 256 j (j < NPR/256), accumulated in TMEM:
                     // 4 nodes (8 doubles, 16 columns) per batch
                     constexpr int NB = 4;
@@ -463,13 +460,9 @@ dvm_status_t launch_gain(dvm_plan_s *P, const double *f, int64_t f_stride, doubl
 {
     *fallback = false;
     // CTAs per group: 16 (N = 64); N = 32 defaults to groups of 8 (more groups walk the
-    // directions in parallel; measured on c4), DVM_G3_CL overrides
+    // directions in parallel; measured on c4), dvm_set_tuning("g3_cl") overrides
     int CL = N == 32 ? 8 : 16;
-    if (N == 32 && getenv("DVM_G3_CL")) CL = atoi(getenv("DVM_G3_CL"));
-    if (!(CL == 16 || (N == 32 && (CL == 8 || CL == 4)))) {
-        set_error("DVM_G3_CL (N = 32): 16, 8 or 4");
-        return DVM_E_UNSUPPORTED;
-    }
+    if (N == 32 && P->tune.g3_cl) CL = P->tune.g3_cl;
     auto kern = CL == 16 ? k_gain3d<N, 16> : CL == 8 ? k_gain3d<N, (N == 32 ? 8 : 16)> : k_gain3d<N, (N == 32 ? 4 : 16)>;
     const size_t smem = gain_smem_bytes(N);
     DVM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -482,8 +475,11 @@ dvm_status_t launch_gain(dvm_plan_s *P, const double *f, int64_t f_stride, doubl
         *fallback = true;
         return DVM_OK;
     }
+    // every CTA allocates all 512 TMEM columns: one CTA per SM, whatever the occupancy
+    // calculator would allow (a second resident CTA would block in tcgen05.alloc)
+    per_sm = 1;
     int max_groups = (sms * per_sm) / CL;
-    if (getenv("DVM_G3_GROUPS")) max_groups = std::max(1, std::min(max_groups, atoi(getenv("DVM_G3_GROUPS"))));
+    if (P->tune.max_groups) max_groups = std::max(1, std::min(max_groups, P->tune.max_groups));
     const int nloc = (int)P->local.size();
     const int64_t nodes = (int64_t)N * N * N;
     const int64_t npairs = (ncells + 1) / 2;
@@ -521,8 +517,7 @@ dvm_status_t launch_gain(dvm_plan_s *P, const double *f, int64_t f_stride, doubl
     a.Tbuf = w.g3_t;
     a.ctr = w.g3_ctr;
     a.H = P->pk.H;
-    a.dbg = getenv("DVM_G3_DEBUG") ? atoi(getenv("DVM_G3_DEBUG")) : 0;
-    if (getenv("DVM_VERBOSE"))
+    if (P->tune.verbose)
         fprintf(stderr, "[dvm] gain3d N=%d: %d groups x %d CTAs, %d chunks, smem %zu\n", N, ngroups, CL, nchunks,
                 smem);
     {

@@ -129,6 +129,18 @@ struct WeightTables {
 };
 }  // namespace dvm
 
+namespace dvm {
+// Tuning and timing switches (dvm_set_tuning; never read from the environment).
+// None changes Q beyond fp64 summation order except fg_dbg / g3_dbg, which
+// skip work for timing experiments and are rejected unless set explicitly.
+struct Tuning {
+    int fg_dbg = 0;      // k_fg2 timing bits: 1 skip B work, 2 skip A work, 4 skip taps (results wrong)
+    int max_groups = 0;  // cap on concurrent cell groups of the persistent 3D kernels (0: all that fit)
+    int g3_cl = 0;       // frame-plane kernel CTAs per group at N = 32 (0: 8)
+    int verbose = 0;     // launch geometry on stderr
+};
+}  // namespace dvm
+
 struct dvm_plan_s {
     int d, N, p, Nbar, Ntilde, kernel, device;
     double L, h;
@@ -148,6 +160,7 @@ struct dvm_plan_s {
     uint64_t launches = 0;
     size_t table_bytes = 0;
     bool profiling = false;
+    dvm::Tuning tune;
     int path_mode = 0;      // evaluation path: 0 auto, 1 v1 orbit sweeps, 2 gain3d/pair2d when built, 3 spectral, 4 FFT gain (3D N = 64)
     bool use_graphs = true; // time steppers replay one captured step (CUDA graph)
     cudaStream_t gstream = nullptr;      // plan-owned stream for graph capture/replay

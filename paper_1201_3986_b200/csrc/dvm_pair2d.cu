@@ -22,6 +22,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <mutex>
 #include <vector>
 
 #include "dvm_internal.h"
@@ -266,18 +267,23 @@ dvm_status_t collide_small2d(dvm_plan_s *P, const double *f, int64_t f_stride, d
     const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>({ncells, 65535, (int64_t)((256ull << 20) / (sizeof(double) * (uint64_t)nunits * nodes))}));
     if ((st = grow(&w.p2_part, &w.p2_part_elems, (size_t)(chunk * nunits * nodes), P->stream))) return st;
     const size_t smem = sizeof(double) * 2 * nodes;
-    static bool attr_set = false;  // the 64 KB opt-in, once per process (host time of small calls)
-    if (!attr_set) {
-        DVM_CUDA(cudaFuncSetAttribute(k_small2d, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)(sizeof(double) * 2 * 64 * 64)));
-        attr_set = true;
-    }
     const Unit2D *units = reinterpret_cast<const Unit2D *>(P->g.units);
     int sms = 148;
     {
         int dev = 0;
         DVM_CUDA(cudaGetDevice(&dev));
         DVM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        // the 64 KB shared-memory opt-in is a per-device (per-context) attribute:
+        // set once per device, under a lock (plans on several devices / threads)
+        static std::mutex mu;
+        static std::vector<char> done;
+        std::lock_guard<std::mutex> lk(mu);
+        if ((int)done.size() <= dev) done.resize(dev + 1, 0);
+        if (!done[dev]) {
+            DVM_CUDA(cudaFuncSetAttribute(k_small2d, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)(sizeof(double) * 2 * 64 * 64)));
+            done[dev] = 1;
+        }
     }
     for (int64_t c0 = 0; c0 < ncells; c0 += chunk) {
         const int nc = (int)std::min<int64_t>(chunk, ncells - c0);

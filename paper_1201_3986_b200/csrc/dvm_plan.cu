@@ -450,7 +450,7 @@ dvm_status_t build_table(dvm_plan_s *P)
     DVM_CUDA(cudaStreamSynchronize(P->stream));
     if ((st = build_gain3d(P))) return st;
     if ((st = build_pair2d(P))) return st;
-    P->table_bytes = acc + P->g.bytes;
+    P->table_bytes = acc;  // plan tables; dvm_plan_info adds the path tables (g.bytes, grown lazily)
     return DVM_OK;
 }
 

@@ -83,6 +83,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "dvm_profile_name": ([ctypes.c_int], ctypes.c_char_p),
         "dvm_set_path": ([P, ctypes.c_int], ctypes.c_int),
         "dvm_set_weights": ([P, V, V], ctypes.c_int),
+        "dvm_set_tuning": ([P, ctypes.c_char_p, ctypes.c_int], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -251,8 +252,13 @@ class Plan:
         _check(load().dvm_set_graphs(self._h, 1 if enable else 0), "dvm_set_graphs")
 
     def set_path(self, path: int):
-        """0 = auto, 1 = v1 orbit sweeps, 2 = FFT-loss kernels, 3 = spectral reference."""
+        """0 = auto, 1 = v1 orbit sweeps, 2 = FFT-loss kernels (gain3d / pair2d),
+        3 = spectral reference, 4 = 3D N = 64 FFT gain, 5 = 2D small-grid pairs."""
         _check(load().dvm_set_path(self._h, int(path)), "dvm_set_path")
+
+    def set_tuning(self, key: str, value: int):
+        """dvm_set_tuning: "max_groups", "g3_cl", "verbose", "timing_dbg" (timing only: Q wrong)."""
+        _check(load().dvm_set_tuning(self._h, key.encode(), int(value)), "dvm_set_tuning")
 
     def set_weights(self, a_box=None, b_box=None):
         """General decoupled weights a(k), b(l) (eq:decoup) as host arrays of shape
