@@ -138,6 +138,27 @@ DVM_API dvm_status_t dvm_collide(dvm_plan_t plan, const double *f, double *Q);
 DVM_API dvm_status_t dvm_collide_batched(dvm_plan_t plan, const double *f, double *Q, int64_t ncells,
                                  int64_t cell_stride);
 
+/* Space-dependent N̄ ("the parameter N̄ can be made space
+ * dependent ... some regions in space deserve less accuracy than others, being
+ * close to equilibrium"): cell c of the batch is evaluated with
+ * plans[level[c]], i.e. Q_c = D^{Ñ,N̄_l}(f_c, f_c) with N̄_l the order of that
+ * plan (eq:decD, with the direction truncation of order N̄_l).
+ *   plans:  nlevels (1..64) plans that differ only in N̄ (same d, N, Ñ, L,
+ *           kernel, device, stream and shard; DVM_E_STATE otherwise).
+ *   f, Q:   DEVICE arrays as in dvm_collide_batched (cell_stride 0 -> N^d).
+ *   level:  DEVICE array of ncells int32, level[c] in [0, nlevels).
+ * The cells are bucketed by level on the device (stable, ascending cell index
+ * within a bucket), each bucket is gathered into the workspace of plans[0],
+ * evaluated as one batch with its plan and scattered back; a bucket holding
+ * the whole batch is evaluated in place.  Synchronises once (the bucket sizes
+ * are read back to size the launches).  Each cell's Q equals a batched
+ * evaluation of that cell with its plan to rounding (the 3D FFT paths pair
+ * cells within a bucket).  Errors: DVM_E_NULL, DVM_E_SHAPE (bad nlevels,
+ * ncells, stride, or a level out of range: Q unspecified), DVM_E_ALIAS,
+ * DVM_E_STATE, DVM_E_NOMEM, DVM_E_CUDA. */
+DVM_API dvm_status_t dvm_collide_batched_levels(const dvm_plan_t *plans, int nlevels, const double *f, double *Q,
+                                                int64_t ncells, int64_t cell_stride, const int *level);
+
 /* End-to-end variant with HOST buffers: copies f to the device, evaluates and
  * copies Q back (pinned host memory recommended); synchronous. */
 DVM_API dvm_status_t dvm_collide_batched_host(dvm_plan_t plan, const double *f_host, double *Q_host,

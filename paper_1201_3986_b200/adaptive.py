@@ -4,20 +4,22 @@ regions in space deserve less accuracy than others, being close to
 equilibrium").
 
 One plan per N̄ level, all with the same Ñ (so the operators differ only in
-the direction truncation of eq:decD); the cells of a batch are bucketed by
-level with libdvm's dvm_copy_cells (device gather/scatter), each bucket is one
-batched evaluation.  Argument marshalling only: every step runs in libdvm.
+the direction truncation of eq:decD).  Evaluation is one call of the C ABI's
+dvm_collide_batched_levels: libdvm buckets the cells by level on the device,
+evaluates each bucket as one batch with its plan and scatters Q back.  This
+module only marshals arguments.
 
 `equilibrium_levels` is a reference policy (not part of the operator): the
 relative L1 distance of each cell to the lattice Maxwellian with its moments.
 """
 from __future__ import annotations
 
+import ctypes
 from typing import Sequence
 
 import numpy as np
 
-from .dvm import Plan
+from .dvm import Plan, _check, _dptr, _stream_ptr, load
 
 
 class AdaptiveNbar:
@@ -32,41 +34,44 @@ class AdaptiveNbar:
         for nb in levels[:-1]:
             self.plans[nb] = Plan(d, N, nb, Ntilde=self.Ntilde, **plan_kw)
         self.d, self.N, self.nodes = d, N, probe.nodes
-        self._buf = None
+        self._handles = (ctypes.c_void_p * len(levels))(*[self.plans[nb]._h.value for nb in levels])
 
     def directions(self) -> dict:
         return {nb: p.A for nb, p in self.plans.items()}
 
     def collide(self, f, nbar_per_cell, out=None):
         """Q for f [cells, N^d] (CUDA float64) with cell c evaluated at N̄ =
-        nbar_per_cell[c] (host sequence of values from `levels`)."""
+        nbar_per_cell[c] (host sequence or CUDA int tensor of values from `levels`)."""
         import torch
-        nb = np.asarray(nbar_per_cell, dtype=np.int64).reshape(-1)
+        if not isinstance(f, torch.Tensor) or not f.is_cuda or f.dtype != torch.float64 or not f.is_contiguous():
+            raise TypeError("f must be a contiguous CUDA float64 tensor")
         ncells = f.numel() // self.nodes
-        if nb.size != ncells:
+        if f.numel() != ncells * self.nodes:
+            raise ValueError(f"f.numel() must be a multiple of N^d = {self.nodes}")
+        lut = {nb: i for i, nb in enumerate(self.levels)}
+        if isinstance(nbar_per_cell, torch.Tensor):
+            nb = nbar_per_cell.to(device=f.device, dtype=torch.int64).reshape(-1)
+            table = torch.full((max(self.levels) + 1,), -1, dtype=torch.int32, device=f.device)
+            for v, i in lut.items():
+                table[v] = i
+            level = table[nb.clamp(0, max(self.levels))].masked_fill((nb < 0) | (nb > max(self.levels)), -1)
+        else:
+            nbh = np.asarray(nbar_per_cell, dtype=np.int64).reshape(-1)
+            bad = set(np.unique(nbh).tolist()) - set(self.levels)
+            if bad:
+                raise ValueError(f"N̄ values {sorted(bad)} are not levels of this plan set")
+            level = torch.from_numpy(np.array([lut[int(v)] for v in nbh], dtype=np.int32)).to(f.device)
+        if level.numel() != ncells:
             raise ValueError("one N̄ per cell")
-        bad = set(np.unique(nb).tolist()) - set(self.levels)
-        if bad:
-            raise ValueError(f"N̄ values {sorted(bad)} are not levels of this plan set")
+        level = level.to(torch.int32).contiguous()
         if out is None:
             out = torch.empty_like(f)
-        if self._buf is None or self._buf[0].numel() < f.numel():
-            self._buf = (torch.empty_like(f), torch.empty_like(f))
-        fb, qb = self._buf
-        for level in self.levels:
-            cells = np.nonzero(nb == level)[0]
-            if cells.size == 0:
-                continue
-            p = self.plans[level]
-            if cells.size == ncells:
-                p.collide(f, out)
-                continue
-            idx = torch.from_numpy(cells).to(f.device)
-            n = int(cells.size)
-            p.copy_cells(f, idx, fb, None, n)
-            fv, qv = fb[: n * self.nodes], qb[: n * self.nodes]
-            p.collide(fv, qv)
-            p.copy_cells(qv, None, out, idx, n)
+        lib = load()
+        for p in self.plans.values():
+            _check(lib.dvm_set_stream(p._h, _stream_ptr()), "dvm_set_stream")
+        _check(lib.dvm_collide_batched_levels(ctypes.cast(self._handles, ctypes.c_void_p), len(self.levels),
+                                              _dptr(f), _dptr(out), ncells, 0, _dptr(level)),
+               "dvm_collide_batched_levels")
         return out
 
 

@@ -227,6 +227,8 @@ dvm_status_t dvm_plan_info(dvm_plan_t P, dvm_plan_info_t *info)
     bytes += sizeof(double) * (w.p2_scr_elems + w.p2_part_elems);
     bytes += sizeof(double) * (size_t)nd * ((w.qtmp ? 1 : 0) + (w.f1tmp ? 1 : 0));
     bytes += sizeof(double) * (kMaxD + 2) * w.mom_rows;
+    bytes += sizeof(double) * (w.lv_f_elems + w.lv_q_elems) + sizeof(int64_t) * w.lv_idx_elems +
+             sizeof(int) * w.lv_cnt_elems;
     info->workspace_bytes = bytes;
     info->launches = P->launches;
     return DVM_OK;
@@ -291,6 +293,36 @@ dvm_status_t dvm_collide_batched(dvm_plan_t P, const double *f, double *Q, int64
     dvm_status_t st = check_batch(P, f, Q, ncells, &cell_stride);
     if (st) return st;
     return collide_batched(P, f, Q, ncells, cell_stride);
+}
+
+dvm_status_t dvm_collide_batched_levels(const dvm_plan_t *plans, int nlevels, const double *f, double *Q,
+                                        int64_t ncells, int64_t cell_stride, const int *level)
+{
+    if (!plans || nlevels < 1 || (ncells > 0 && !level)) {
+        set_error(nlevels < 1 ? "nlevels must be >= 1" : "NULL argument");
+        return nlevels < 1 ? DVM_E_SHAPE : DVM_E_NULL;
+    }
+    if (nlevels > 64) {
+        set_error("at most 64 levels");
+        return DVM_E_SHAPE;
+    }
+    for (int i = 0; i < nlevels; ++i) {
+        const dvm_plan_s *a = plans[0], *b = plans[i];
+        if (!b) {
+            set_error("NULL plan");
+            return DVM_E_NULL;
+        }
+        if (b->d != a->d || b->N != a->N || b->Ntilde != a->Ntilde || b->L != a->L || b->kernel != a->kernel ||
+            b->device != a->device || b->stream != a->stream || b->shard_world != a->shard_world ||
+            b->shard_rank != a->shard_rank) {
+            set_error("dvm_collide_batched_levels: the plans must share d, N, Ñ, L, kernel, device, stream and "
+                      "shard (they may differ only in N̄)");
+            return DVM_E_STATE;
+        }
+    }
+    dvm_status_t st = check_batch(plans[0], f, Q, ncells, &cell_stride);
+    if (st) return st;
+    return collide_levels(plans, nlevels, f, Q, ncells, cell_stride, level);
 }
 
 dvm_status_t dvm_collide(dvm_plan_t P, const double *f, double *Q)

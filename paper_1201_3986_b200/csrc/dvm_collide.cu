@@ -21,6 +21,8 @@
 // the fastest axis whenever the orbit vector has an odd non-fastest component.
 #include <algorithm>
 
+#include <vector>
+
 #include "dvm_internal.h"
 
 namespace dvm {
@@ -268,6 +270,55 @@ __global__ void k_copy_cells(const double *__restrict__ src, const int64_t *__re
     }
 }
 
+// strided variant: dst cell di[c] (stride dst_stride) = src cell si[c] (stride src_stride)
+__global__ void k_copy_cells_strided(const double *__restrict__ src, int64_t src_stride, const int64_t *__restrict__ si,
+                                     double *__restrict__ dst, int64_t dst_stride, const int64_t *__restrict__ di,
+                                     int64_t ncells, int64_t nodes)
+{
+    const int64_t total = ncells * nodes;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = i / nodes, x = i % nodes;
+        const int64_t a = si ? si[c] : c, b = di ? di[c] : c;
+        dst[b * dst_stride + x] = src[a * src_stride + x];
+    }
+}
+
+// Space-dependent N̄: stable bucketing of the cells by level on the device.
+// idx[] receives the cells of level 0 in ascending order, then level 1, ...;
+// cnt[lv] the bucket sizes and cnt[nlevels] the number of cells whose level is
+// out of [0, nlevels).  One block; every count is an exact integer.
+__global__ void k_level_bucket(const int *__restrict__ level, int64_t ncells, int nlevels, int64_t *__restrict__ idx,
+                               int *__restrict__ cnt)
+{
+    __shared__ int warp_tot[32];
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5, nw = blockDim.x >> 5;
+    int64_t base = 0;
+    for (int lv = -1; lv < nlevels; ++lv) {  // lv = -1: cells with an invalid level (counted only)
+        int64_t n = 0;
+        for (int64_t c0 = 0; c0 < ncells; c0 += blockDim.x) {
+            const int64_t c = c0 + t;
+            bool flag = false;
+            if (c < ncells) {
+                const int v = level[c];
+                flag = lv < 0 ? (v < 0 || v >= nlevels) : v == lv;
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, flag);
+            if (lane == 0) warp_tot[w] = __popc(m);
+            __syncthreads();
+            int off = 0, tot = 0;
+            for (int k = 0; k < nw; ++k) {
+                off += k < w ? warp_tot[k] : 0;
+                tot += warp_tot[k];
+            }
+            if (flag && lv >= 0) idx[base + n + off + __popc(m & ((1u << lane) - 1u))] = c;
+            n += tot;
+            __syncthreads();
+        }
+        if (t == 0) cnt[lv < 0 ? nlevels : lv] = (int)n;
+        if (lv >= 0) base += n;
+    }
+}
+
 // TVD-RK2 (Heun) stages: f1 = f + dt q ; f = (f + f1 + dt q1) / 2
 __global__ void k_rk2_stage1(const double *f, const double *q, double dt, double *f1, int64_t n)
 {
@@ -486,6 +537,52 @@ dvm_status_t copy_cells(dvm_plan_s *P, const double *src, const int64_t *si, dou
     return DVM_OK;
 }
 
+dvm_status_t collide_levels(dvm_plan_s *const *plans, int nlevels, const double *f, double *Q, int64_t ncells,
+                            int64_t stride, const int *level)
+{
+    dvm_plan_s *P0 = plans[0];
+    const Geo g = geo_of(P0);
+    if (ncells == 0) return DVM_OK;
+    Workspace &w = P0->ws;
+    dvm_status_t st;
+    if ((st = grow(&w.lv_idx, &w.lv_idx_elems, (size_t)ncells, P0->stream))) return st;
+    if ((st = grow(&w.lv_cnt, &w.lv_cnt_elems, (size_t)nlevels + 1, P0->stream))) return st;
+    {
+        LaunchScope ls(P0, KC_ZERO);
+        k_level_bucket<<<1, 1024, 0, P0->stream>>>(level, ncells, nlevels, w.lv_idx, w.lv_cnt);
+        DVM_CUDA(cudaGetLastError());
+    }
+    std::vector<int> cnt(nlevels + 1);
+    DVM_CUDA(cudaMemcpyAsync(cnt.data(), w.lv_cnt, sizeof(int) * (nlevels + 1), cudaMemcpyDeviceToHost, P0->stream));
+    DVM_CUDA(cudaStreamSynchronize(P0->stream));
+    if (cnt[nlevels] != 0) {
+        set_error("dvm_collide_batched_levels: a cell's level is outside [0, nlevels)");
+        return DVM_E_SHAPE;
+    }
+    int64_t off = 0;
+    for (int lv = 0; lv < nlevels; ++lv) {
+        const int64_t n = cnt[lv];
+        if (n == 0) continue;
+        if (n == ncells) return collide_batched(plans[lv], f, Q, ncells, stride);  // one level: no gather
+        if ((st = grow(&w.lv_f, &w.lv_f_elems, (size_t)n * g.nodes, P0->stream))) return st;
+        if ((st = grow(&w.lv_q, &w.lv_q_elems, (size_t)n * g.nodes, P0->stream))) return st;
+        const int64_t *ix = w.lv_idx + off;
+        {
+            LaunchScope ls(P0, KC_ZERO);
+            k_copy_cells_strided<<<592, kThreads, 0, P0->stream>>>(f, stride, ix, w.lv_f, g.nodes, nullptr, n, g.nodes);
+            DVM_CUDA(cudaGetLastError());
+        }
+        if ((st = collide_batched(plans[lv], w.lv_f, w.lv_q, n, g.nodes))) return st;
+        {
+            LaunchScope ls(P0, KC_ZERO);
+            k_copy_cells_strided<<<592, kThreads, 0, P0->stream>>>(w.lv_q, g.nodes, nullptr, Q, stride, ix, n, g.nodes);
+            DVM_CUDA(cudaGetLastError());
+        }
+        off += n;
+    }
+    return DVM_OK;
+}
+
 dvm_status_t rk2_stage(dvm_plan_s *P, int stage, double *f, double *f1, const double *q, double dt)
 {
     const Geo g = geo_of(P);
@@ -524,7 +621,7 @@ void free_workspace(dvm_plan_s *P)
 {
     clear_profile(P);
     Workspace &w = P->ws;
-    void *ptrs[] = {w.S, w.part, w.f_stage, w.q_stage, w.mom_partial, w.mom_dev, w.qtmp, w.f1tmp, w.mom_ctr, w.fft_z, w.g3_f, w.g3_t, w.g3_q, w.g3_ctr, w.p2_scr, w.p2_part, w.sp_z, w.fg_fhat};
+    void *ptrs[] = {w.S, w.part, w.f_stage, w.q_stage, w.mom_partial, w.mom_dev, w.qtmp, w.f1tmp, w.mom_ctr, w.fft_z, w.g3_f, w.g3_t, w.g3_q, w.g3_ctr, w.p2_scr, w.p2_part, w.sp_z, w.fg_fhat, w.lv_f, w.lv_q, w.lv_idx, w.lv_cnt};
     for (void *q : ptrs)
         if (q) cudaFree(q);
     w = Workspace{};

@@ -84,6 +84,10 @@ struct Workspace {
     size_t sp_z_elems = 0;
     double2 *fg_fhat = nullptr;     // FFT gain: f̂ of the cell pairs [pairs][nodes]
     size_t fg_fhat_elems = 0;
+    double *lv_f = nullptr, *lv_q = nullptr;  // per-cell N̄: gathered cells of one level and their Q
+    int64_t *lv_idx = nullptr;                // per-cell N̄: cells bucketed by level
+    int *lv_cnt = nullptr;                    // per-cell N̄: bucket sizes (+ invalid count)
+    size_t lv_f_elems = 0, lv_q_elems = 0, lv_idx_elems = 0, lv_cnt_elems = 0;
 };
 
 }  // namespace dvm
@@ -238,6 +242,8 @@ dvm_status_t moments(dvm_plan_s *P, const double *f, double *dev_out_row);
 dvm_status_t axpy(dvm_plan_s *P, double *f, const double *q, double dt);
 dvm_status_t moments_ctr(dvm_plan_s *P, const double *f, double *dev_base, int *dev_ctr);
 dvm_status_t rk2_stage(dvm_plan_s *P, int stage, double *f, double *f1, const double *q, double dt);
+dvm_status_t collide_levels(dvm_plan_s *const *plans, int nlevels, const double *f, double *Q, int64_t ncells,
+                            int64_t stride, const int *level);
 dvm_status_t copy_cells(dvm_plan_s *P, const double *src, const int64_t *si, double *dst, const int64_t *di,
                         int64_t ncells);
 dvm_status_t zero_cells(dvm_plan_s *P, double *Q, int64_t q_stride, int64_t ncells, int64_t nodes);

@@ -84,6 +84,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "dvm_set_path": ([P, ctypes.c_int], ctypes.c_int),
         "dvm_set_weights": ([P, V, V], ctypes.c_int),
         "dvm_set_tuning": ([P, ctypes.c_char_p, ctypes.c_int], ctypes.c_int),
+        "dvm_collide_batched_levels": ([V, ctypes.c_int, V, V, I64, I64, V], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
