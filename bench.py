@@ -1,16 +1,24 @@
 #!/usr/bin/env python3
 """Benchmark of the hot path: Q(f,f) evaluations/s at d=3 N=64 N̄=8 (fp64),
 BASELINE.json's metric, on config c5 (512 spatial cells of perturbed
-Maxwellians per GPU, batched in one dvm_collide_batched call).
+Maxwellians, batched dvm_collide_batched calls).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload c1|c2|c3|c4|c5] [--scaling strong|weak]
   torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU)
 
-A step = one full evaluation of all 512 cells of this rank (all 2017
-directions).  Multi-GPU: cells are sharded by rank (weak scaling: every rank
-owns 512 cells of a global batch of 512*N, no data-path collective), timed on
-the device between barriers, max over ranks.  Inputs (1 GiB per rank) are
-larger than the 126 MB L2, so no explicit flush is needed between steps.
+c5 (default): a step = one full evaluation of the 512 cells (all 2017
+directions).  Multi-GPU: the 512 cells are sharded into contiguous blocks of
+512/N per rank (--scaling strong, the default, BASELINE c5: "cells sharded
+across 1/2/4/8 GPUs"; no data-path collective); --scaling weak gives every rank
+512 cells of a global batch of 512 N.  Timed on the device between barriers,
+max over ranks.  Inputs (1 GiB at N = 1) exceed the 126 MB L2.
+
+c1-c4 (--workload): one grid per step.  c1, c3, c4: one evaluation; with N > 1
+direction-sharded (2D: whole pair units) with one fp64 NCCL all-reduce inside
+the timed region.  c2: one evaluation + 100 explicit Euler steps dt = 0.01
+(BASELINE c2; 101 evaluations per step, one rank's trajectory; N > 1 runs
+independent replicas).
 
 `--impl reference` times the CPU oracle (oracle/, the slow direct pair sum)
 on a bounded sample of the same workload on the host cores (rank 0 only).
@@ -101,76 +109,144 @@ def _dist():
     return world, rank, local
 
 
-def cpu_baseline(seconds: float = 15.0):
-    """Oracle (oracle/dvm_oracle.c, as it stands) on a bounded sample of c5:
-    the first cells of the batch, a seeded set of nodes per cell; extrapolated
-    to cell-evaluations/s = (nodes/s) / N^3."""
+def _oracle_sample(name: str, seconds: float, seed: int):
+    """Time the oracle (oracle/dvm_oracle.c as it stands) on a bounded sample of
+    workload `name`: whole-grid evaluations when the grid is small, otherwise a
+    seeded set of nodes of one cell sized for ~`seconds` of host work.  The
+    oracle hands out blocks of 16 nodes per thread (OpenMP dynamic), so the
+    sample is a multiple of 16 x threads nodes and every thread is busy.
+    Returns (evals/s, busy threads, sample description, seconds)."""
     import dvm_inputs
     from oracle import oracle
-    nodes = NGRID ** D
-    f = dvm_inputs.make("c5", cells=2)
-    Nt = oracle.ntilde_rule(NGRID, NBAR)
-    rng = np.random.default_rng(0)
-    cores = os.cpu_count() or 1
-    # calibrate, then size the sample for ~`seconds` of CPU work
-    pts = rng.integers(0, nodes, size=max(8, cores)).astype(np.int64)
+    cfg = dvm_inputs.CONFIGS[name]
+    nodes = cfg.N ** cfg.d
+    Nt = oracle.ntilde_rule(cfg.N, cfg.Nbar)
+    f = dvm_inputs.make(name, cells=1)[0]
+    threads = os.cpu_count() or 1
+    block = 16 * threads
+    npairs = oracle.pairs(cfg.d, Nt, cfg.Nbar, 1.0)[2].size
+    if nodes <= 4 * block:
+        t0 = time.perf_counter()
+        oracle.collide(f, cfg.d, cfg.N, cfg.Nbar, Nt, cfg.L, diagnostics=False)
+        dt = time.perf_counter() - t0
+        reps = max(1, min(200, int(seconds / max(dt, 1e-4))))
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            oracle.collide(f, cfg.d, cfg.N, cfg.Nbar, Nt, cfg.L, diagnostics=False)
+        dt = time.perf_counter() - t0
+        busy = min(threads, -(-nodes // 16))
+        return reps / dt, busy, (f"{reps} whole-grid evaluations of {name} ({nodes} nodes, {npairs} pairs/node), "
+                                 f"{dt:.1f} s"), dt
+    rng = np.random.default_rng(seed)
+    pts = np.sort(rng.choice(nodes, size=block, replace=False)).astype(np.int64)
     t0 = time.perf_counter()
-    oracle.collide(f[0], D, NGRID, NBAR, Nt, L, points=pts)
+    oracle.collide(f, cfg.d, cfg.N, cfg.Nbar, Nt, cfg.L, points=pts, diagnostics=False)
     dt = time.perf_counter() - t0
-    n = int(max(cores, min(4 * nodes, len(pts) * seconds / max(dt, 1e-3))))
-    pts = np.sort(rng.integers(0, nodes, size=n)).astype(np.int64)
+    k = int(max(1, min(nodes // block, seconds / max(dt, 1e-3))))
+    pts = np.sort(rng.choice(nodes, size=k * block, replace=False)).astype(np.int64)
     t0 = time.perf_counter()
-    oracle.collide(f[1], D, NGRID, NBAR, Nt, L, points=pts)
+    oracle.collide(f, cfg.d, cfg.N, cfg.Nbar, Nt, cfg.L, points=pts, diagnostics=False)
     dt = time.perf_counter() - t0
-    return {"value": (n / dt) / nodes, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"{n} seeded nodes of c5 cell 1 (of 64^3), direct pair sum "
-                      f"({oracle.pairs(D, Nt, NBAR, 1.0)[2].size} pairs/node), {dt:.1f} s; "
-                      f"evals/s = nodes/s / 64^3"}
+    return ((pts.size / dt) / nodes, threads,
+            f"{pts.size} seeded nodes of one {name} cell (of {nodes}), direct pair sum ({npairs} pairs/node), "
+            f"{dt:.1f} s; evals/s = nodes/s / {nodes}", dt)
+
+
+def cpu_baseline(name: str = "c5", seconds: float = 15.0):
+    value, busy, sample, _ = _oracle_sample(name, seconds, 0)
+    return {"value": value, "unit": UNIT, "cores": busy, "kind": "oracle", "sample": sample}
 
 
 def run_reference(args):
     world, rank, _ = _dist()
     if rank != 0:
         return 0
-    import dvm_inputs
-    from oracle import oracle
-    nodes = NGRID ** D
-    Nt = oracle.ntilde_rule(NGRID, NBAR)
-    f = dvm_inputs.make("c5", cells=1)[0]
-    cores = os.cpu_count() or 1
-    rng = np.random.default_rng(1)
-    # each step: a bounded sample of nodes (sized so the whole run takes ~minutes)
-    per_step = int(os.environ.get("REF_NODES_PER_STEP", str(max(8 * cores, 64))))
+    name = args.workload
+    per_step_s = float(os.environ.get("REF_SECONDS_PER_STEP", "6"))
     for _ in range(args.warmup):
-        oracle.collide(f, D, NGRID, NBAR, Nt, L, points=rng.integers(0, nodes, size=min(per_step, 16)))
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        pts = np.sort(rng.integers(0, nodes, size=per_step)).astype(np.int64)
-        oracle.collide(f, D, NGRID, NBAR, Nt, L, points=pts)
-    dt = time.perf_counter() - t0
-    value = args.steps * per_step / dt / nodes
-    ms_per_step = dt / args.steps * 1e3 * (nodes / per_step)
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        _oracle_sample(name, 0.5, 99)
+    vals, secs = [], 0.0
+    busy, sample = 0, ""
+    for k in range(args.steps):
+        v, busy, sample, dt = _oracle_sample(name, per_step_s, 1 + k)
+        vals.append(v)
+        secs += dt
+    value = float(np.mean(vals))
+    import dvm_inputs
+    cfg = dvm_inputs.CONFIGS[name]
+    evals_per_step = (cfg.cells if name == "c5" else 101 if name == "c2" else 1)
+    ms_per_step = evals_per_step / value * 1e3  # extrapolated: one full step of the workload
+    line = {"impl": "reference", "metric": METRIC if name == "c5" else f"Q(f,f) evals/sec, {name}",
+            "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded, dvm_inputs c5)",
-            "config": {"workload": "c5: d=3 hard spheres N=64 Nbar=8 Ntilde=14 L=8, evaluation of one cell",
-                       "sample_nodes_per_step": per_step},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                             "sample": f"{per_step} seeded nodes of one c5 cell per step, extrapolated: "
-                                       "evals/s = nodes/s / 64^3"},
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": f"synthetic (seeded, dvm_inputs {name})",
+            "config": {"workload": WORKLOADS[name], "sample_per_step": sample,
+                       "timed_host_seconds": secs,
+                       "ms_per_step_note": "extrapolated from the timed sample to one full step of the workload "
+                                           "(the full oracle step is far longer than the driver's run)"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": busy, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
-# what limits the dominant kernel (ncu evidence in profiles/r01/SUMMARY.md)
+WORKLOADS = {
+    "c1": "c1: d=2 Maxwell, N=16, Nbar=4, Ntilde=4, L=8, one grid",
+    "c2": "c2: d=2 Maxwell, N=64, Nbar=8, Ntilde=14, L=8, one evaluation + 100 Euler steps dt=0.01",
+    "c3": "c3: d=2 Maxwell, N=256, Nbar=16, Ntilde=57, L=8, one grid",
+    "c4": "c4: d=3 hard spheres, N=32, Nbar=4, Ntilde=7, L=8, one grid",
+    "c5": "c5: d=3 hard spheres, N=64, Nbar=8, Ntilde=14, L=8, 512 batched cells",
+}
+
+
+def _kernel_metrics(name: str):
+    """ncu evidence for the dominant kernel, measured on bench.py's own launch
+    (profiles/kernel_metrics.json, written from an ncu capture; see profiles/r02)."""
+    path = os.path.join(ROOT, "profiles", "kernel_metrics.json")
+    try:
+        return json.load(open(path)).get(name)
+    except Exception:
+        return None
+
+
+# what limits the dominant kernel (ncu evidence in profiles/r02/SUMMARY.md)
 BINDING = {
-    "k_fgain3d": "latency-bound mix: SM L1/shared data pipe 58% (FFT exchanges, plane/ring staging, tap loads), "
-                 "fp64 pipe 22%, issue 31%; see profiles/r01/SUMMARY.md",
+    "k_fg2": "latency-bound: phase-B tap and ring loads waiting on L2 (long scoreboard), SM L1/shared pipe ~60%, "
+             "fp64 pipe ~24%, issue ~29%; see profiles/r02/SUMMARY.md",
     "k_gain3d": "SM L1/shared-memory pipe (sliding-program loads + scattered frame gather/store); "
                 "see profiles/r01/SUMMARY.md",
 }
+
+
+def _roofline(prof, psteps, bytes_per_eval, evals_per_step, peak_override=None):
+    """roofline object for the dominant kernel: algorithmic (streaming-
+    formulation) bytes of the evaluations one launch covers / its CUDA-event
+    launch time, against the measured HBM copy bandwidth."""
+    total = sum(v[0] for v in prof.values()) or 1.0
+    top_name, (top_ms, top_n) = max(prof.items(), key=lambda kv: kv[1][0])
+    launches_per_step = max(1, top_n // psteps)
+    alg_bytes = bytes_per_eval * evals_per_step / launches_per_step
+    avg_launch_s = top_ms / top_n / 1e3
+    peak, peak_src = _peaks()
+    achieved = alg_bytes / avg_launch_s / 1e9
+    km = _kernel_metrics(top_name) or {}
+    traffic = km.get("dram_bytes_per_launch") if km.get("launch_bytes_match", True) else None
+    r = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+         "traffic": traffic, "kernel": top_name, "kernel_share_of_step": top_ms / total,
+         "kernel_avg_launch_ms": top_ms / top_n, "algorithmic_bytes_per_launch": alg_bytes,
+         "peak_source": peak_src,
+         "note": "streaming-formulation bytes (A+2)*8*N^d per cell-evaluation (SURVEY.md 8(d)); "
+                 "effective, not DRAM traffic",
+         "binding_resource": BINDING.get(top_name, "see profiles/r02/SUMMARY.md")}
+    if km:
+        # SURVEY 8(d)'s other two numbers, from the ncu capture of the same launch
+        if traffic:
+            r["dram_GBps"] = traffic / avg_launch_s / 1e9
+        r["fp64_pipe_pct"] = km.get("fp64_pipe_pct")
+        r["l1tex_pct"] = km.get("l1tex_pct")
+        r["ncu_source"] = km.get("source")
+    return r
 
 
 def run_ours(args):
@@ -179,6 +255,7 @@ def run_ours(args):
 
     import dvm_inputs
     from paper_1201_3986_b200 import Plan
+    from paper_1201_3986_b200.parallel import cell_range
 
     world, rank, local = _dist()
     if world != args.gpus:
@@ -191,10 +268,14 @@ def run_ours(args):
         if world > 1:
             dist.barrier()
 
-    cells = args.cells
     nodes = NGRID ** D
-    # this rank's shard of the global batch (cells rank*cells ... ), weak scaling
-    f_host = dvm_inputs.make("c5", cells=cells, first_cell=rank * cells)
+    if args.scaling == "strong":
+        global_cells = args.cells
+        first, cells = cell_range(global_cells, rank, world)
+    else:
+        global_cells = args.cells * world
+        first, cells = rank * args.cells, args.cells
+    f_host = dvm_inputs.make("c5", cells=cells, first_cell=first)
     f = torch.from_numpy(f_host).cuda()
     Q = torch.empty_like(f)
     plan = Plan(D, NGRID, NBAR)
@@ -204,7 +285,7 @@ def run_ours(args):
     for _ in range(args.warmup):
         plan.collide(f, Q)
     torch.cuda.synchronize()
-    mass_rel = float((Q.sum(dim=1).abs() / Q.abs().sum(dim=1)).max())
+    mass_rel = float((Q.sum(dim=1).abs() / Q.abs().sum(dim=1)).max()) if cells else 0.0
 
     # ---- headline: device-resident inputs, K steps between barriers, CUDA events
     launches0 = plan.launches()
@@ -225,7 +306,7 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
     ms_step = ms_total / args.steps
-    value = world * cells * args.steps / (ms_total / 1e3)
+    value = global_cells * args.steps / (ms_total / 1e3)
 
     # ---- dominant kernel: per-launch CUDA events inside libdvm on the same stream
     plan.profile(True)
@@ -234,35 +315,7 @@ def run_ours(args):
         plan.collide(f, Q)
     prof = plan.profile_read()
     plan.profile(False)
-    prof_total = sum(v[0] for v in prof.values())
-    top = max(prof.items(), key=lambda kv: kv[1][0])
-    top_name, (top_ms, top_n) = top
-    # algorithmic bytes per launch of the dominant kernel: the streaming
-    # formulation charges (A+2)*8*N^3 bytes per cell-evaluation
-    # (one f pass per direction + f read + Q write).  k_gain3d evaluates the
-    # whole batch (all cells, all directions) in one launch per collide; the v1
-    # orbit path launches k_rowsum once per direction chunk.
-    if top_name in ("k_gain3d", "k_fgain3d"):
-        alg_bytes = (A + 2) * 8.0 * nodes * cells * psteps / top_n
-    else:
-        alg_bytes = (A + 2) * 8.0 * nodes * cells * psteps / max(1, prof.get("k_rowsum", (0, 1))[1])
-    avg_launch_s = top_ms / top_n / 1e3
-    peak, peak_src = _peaks()
-    achieved = alg_bytes / avg_launch_s / 1e9
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "traffic_per_launch.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get(top_name)
-        except Exception:
-            traffic = None
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": top_name, "kernel_share_of_step": top_ms / prof_total,
-                "kernel_avg_launch_ms": top_ms / top_n, "algorithmic_bytes_per_launch": alg_bytes,
-                "peak_source": peak_src,
-                "note": "streaming-formulation bytes (A+2)*8*N^3 per cell-evaluation (SURVEY.md 8(d)); "
-                        "effective, not DRAM traffic",
-                "binding_resource": BINDING.get(top_name, "see profiles/r01/SUMMARY.md")}
+    roofline = _roofline(prof, psteps, (A + 2) * 8.0 * nodes, cells)
     eff_step_gbs = value / world * (A + 2) * 8.0 * nodes / 1e9
 
     # ---- e2e through the C ABI with host buffers (pinned), copies inside the timed region
@@ -280,19 +333,19 @@ def run_ours(args):
         t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    e2e_value = world * cells * e2e_steps / (e2e_ms / 1e3)
+    e2e_value = global_cells * e2e_steps / (e2e_ms / 1e3)
     same = bool(torch.equal(qh, Q.cpu()))
 
     clocks = clk.summary()
-    line = None
     if rank == 0:
-        cpu = cpu_baseline() if (world == 1 and not args.no_cpu_baseline) else None
+        cpu = cpu_baseline("c5") if (world == 1 and not args.no_cpu_baseline) else None
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded c5 Maxwellian cells, dvm_inputs)",
-                "config": {"workload": "c5: d=3 hard spheres, N=64, Nbar=8, Ntilde=14, L=8, batched cells",
-                           "cells_per_rank": cells, "global_cells": cells * world, "directions": A,
-                           "parallelism": f"cell-sharded x{world}", "l2_flush": "inputs 1 GiB/rank > 126 MB L2",
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+                "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded c5 Maxwellian cells, dvm_inputs)",
+                "config": {"workload": WORKLOADS["c5"], "global_cells": global_cells, "cells_rank0": cells,
+                           "directions": A, "parallelism": f"cell-sharded x{world} ({args.scaling})",
+                           "l2_flush": "inputs 1 GiB (N=1) > 126 MB L2",
                            "effective_streaming_GBps_per_gpu": eff_step_gbs},
                 "roofline": roofline, "cpu_baseline": cpu,
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(fh.numel() * 8),
@@ -307,54 +360,126 @@ def run_ours(args):
     return 0
 
 
-def run_c3(args):
-    """BASELINE c3 (2D, N=256, N̄=16, one grid): direction-sharded over the
-    ranks (LPT share per rank) with one fp64 NCCL sum
-    all-reduce of the N^2 result inside the timed region (strong scaling)."""
+def run_grid(args):
+    """c1-c4: one grid per step.  c1/c3/c4: one evaluation (N > 1: direction-
+    sharded, 2D by pair units, + one fp64 NCCL sum all-reduce inside the timed
+    region); c2: one evaluation + 100 Euler steps on the
+    device (CUDA-graph replay), per rank (N > 1: independent replicas)."""
     import torch
     import torch.distributed as dist
 
     import dvm_inputs
+    from paper_1201_3986_b200 import Plan
     from paper_1201_3986_b200.parallel import DirectionSharded
 
+    name = args.workload
+    cfg = dvm_inputs.CONFIGS[name]
     world, rank, local = _dist()
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    cfg = dvm_inputs.CONFIGS["c3"]
-    f = torch.from_numpy(dvm_inputs.make("c3")).cuda()
+    f0 = dvm_inputs.make(name)
+    nodes = cfg.N ** cfg.d
+    f = torch.from_numpy(f0).cuda()
     q = torch.empty_like(f)
-    ev = DirectionSharded(cfg.d, cfg.N, cfg.Nbar)
+    c2 = name == "c2"
+    if c2:
+        ev = None
+        plan = Plan(cfg.d, cfg.N, cfg.Nbar)
+        fw = f.clone()
+
+        def step():
+            fw.copy_(f)
+            plan.collide(fw, q)
+            plan.euler(fw, 0.01, 100)
+        evals = 101
+    else:
+        ev = DirectionSharded(cfg.d, cfg.N, cfg.Nbar)
+        plan = ev.plan
+
+        def step():
+            ev(f, q)
+        evals = 1
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
-        ev(f, q)
+        step()
     torch.cuda.synchronize()
-    reps = max(20, args.steps)
+    reps = max(20, args.steps) if not c2 else max(3, args.steps)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    launches0 = plan.launches()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         e0.record(stream)
         for _ in range(reps):
-            ev(f, q)
+            step()
         e1.record(stream)
         torch.cuda.synchronize()
+    launches = (plan.launches() - launches0) // reps
     ms = e0.elapsed_time(e1) / reps
     if world > 1:
+        dist.barrier()
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    A_local = ev.plan.info()["A_local"]
+    value = (world if c2 else 1) * evals * 1e3 / ms
+    A = plan.A
+    plan.profile(True)
+    psteps = 2
+    for _ in range(psteps):
+        step()
+    prof = plan.profile_read()
+    plan.profile(False)
+    roofline = _roofline(prof, psteps, (A + 2) * 8.0 * nodes, evals)
+    # e2e with host buffers through the C ABI: f in, Q (and for c2 the final f) out
+    fh = torch.from_numpy(f0.copy()).pin_memory()
+    qh = torch.empty_like(fh).pin_memory()
+    if c2:
+        def e2e():
+            fw.copy_(fh, non_blocking=True)
+            plan.collide(fw, q)
+            plan.euler(fw, 0.01, 100)
+            qh.copy_(q, non_blocking=True)
+            fh.copy_(fw, non_blocking=True)
+            torch.cuda.synchronize()
+            fh.copy_(torch.from_numpy(f0))
+        h2d, d2h = fh.numel() * 8, 2 * fh.numel() * 8
+    else:
+        def e2e():
+            if world > 1:
+                f.copy_(fh, non_blocking=True)
+                ev(f, q)
+                qh.copy_(q, non_blocking=True)
+                torch.cuda.synchronize()
+            else:
+                plan.collide_host_ptr(fh.data_ptr(), qh.data_ptr(), 1)
+        h2d, d2h = fh.numel() * 8, fh.numel() * 8
+    e2e()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        e2e()
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / reps
+    if world > 1:
+        t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
     if rank == 0:
-        line = {"metric": "Q(f,f) evals/sec, c3 (d=2 N=256 N̄=16, one grid, direction-sharded)", "value": 1e3 / ms,
-                "unit": "evals/s", "n_gpus": world, "steps": reps, "warmup": args.warmup, "ms_per_step": ms,
-                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic (seeded c3 4-bump mixture, dvm_inputs)",
-                "config": {"workload": "c3", "directions": ev.plan.A, "directions_rank0": A_local,
-                           "parallelism": f"direction-sharded x{world} + NCCL all-reduce",
-                           "l2_flush": "none (c3 fits L2; strong-scaling latency figure)"},
-                "clocks": clk.summary()}
+        cpu = cpu_baseline(name, 8.0) if (world == 1 and not args.no_cpu_baseline) else None
+        par = ("replicas" if c2 else "direction-sharded (2D: pair units) + NCCL all-reduce") + f" x{world}"
+        line = {"metric": f"Q(f,f) evals/sec, {name}", "value": value, "unit": UNIT, "n_gpus": world,
+                "steps": reps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+                "scaling": "weak" if c2 else "strong", "vs_baseline": None, "dtype": "f64",
+                "data": f"synthetic (seeded {name}, dvm_inputs)",
+                "config": {"workload": WORKLOADS[name], "evals_per_step": evals, "directions": A,
+                           "directions_rank0": plan.info()["A_local"], "parallelism": par,
+                           "l2_flush": "none: the grid fits L2 (latency-bound single-grid figure)"},
+                "roofline": roofline, "cpu_baseline": cpu,
+                "e2e": {"value": (world if c2 else 1) * evals * 1e3 / e2e_ms, "unit": UNIT,
+                        "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+                "gpu_launches": int(launches), "clocks": clk.summary(),
+                "kernel_profile_ms": {k: v[0] / psteps for k, v in prof.items() if v[1]}}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -368,18 +493,20 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cells", type=int, default=CELLS_PER_RANK)
+    ap.add_argument("--cells", type=int, default=CELLS_PER_RANK,
+                    help="c5: global cells (strong) or cells per rank (weak)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", default="c5", choices=["c5", "c3"],
-                    help="c5 (default, the BASELINE metric) or c3 (direction-sharded single grid)")
+    ap.add_argument("--workload", default="c5", choices=["c1", "c2", "c3", "c4", "c5"],
+                    help="c5 (default, the BASELINE metric) or one of the single-grid configs")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("note: --warmup raised to 3 (timing rules)", file=sys.stderr)
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
-    if args.workload == "c3":
-        return run_c3(args)
+    if args.workload != "c5":
+        return run_grid(args)
     return run_ours(args)
 
 

@@ -127,14 +127,25 @@ DVM_API dvm_status_t dvm_plan_geometry(dvm_plan_t plan, int idx, int *u, int *w,
 /* Change the stream used by subsequent calls (cudaStream_t as void*). */
 DVM_API dvm_status_t dvm_set_stream(dvm_plan_t plan, void *stream);
 
-/* Q = D^{Ñ,N̄}(f,f) for one cell: f, Q device arrays of N^d doubles.  For a
- * sharded plan, Q is the partial sum over this shard's directions. */
+/* Q = D^{Ñ,N̄}(f,f) for one cell (eq:decD: the gain
+ * a_e S_e T_e and loss a_e f U_e summed over the lines e of order <= N̄,
+ * PAPER.md:796-827; equal to the direct pair sum of eq:DR, PAPER.md:386-390,
+ * restricted to those lines).  f, Q: caller-owned DEVICE arrays of N^d doubles
+ * (layout above), Q must not overlap f.  For a sharded plan Q is the partial
+ * sum over this shard's directions; the caller sums the
+ * shards.  Asynchronous on the plan's stream.  Errors: DVM_E_NULL (plan, f or
+ * Q NULL), DVM_E_ALIAS (overlap), DVM_E_NOMEM (workspace), DVM_E_CUDA. */
 DVM_API dvm_status_t dvm_collide(dvm_plan_t plan, const double *f, double *Q);
 
-/* Same for ncells cells; cell c occupies [c*cell_stride, c*cell_stride + N^d)
- * of f and of Q (cell_stride 0 -> N^d).  The plan grows a device workspace on
- * first use of a batch size (3D: ~2 × 16 B per node per cell pair plus a 256 MiB
- * FFT batch; 2D: ≤ 512 MiB of per-pair partials); DVM_E_NOMEM if it cannot. */
+/* The same operator for ncells independent spatial cells (the
+ * space-inhomogeneous setting: the collision step is local
+ * in space, one evaluation per cell); cell c occupies [c*cell_stride,
+ * c*cell_stride + N^d) of f and of Q (cell_stride 0 -> N^d; f and Q DEVICE,
+ * caller-owned, non-overlapping).  ncells = 0 is a no-op.  Errors as
+ * dvm_collide plus DVM_E_SHAPE (ncells < 0, cell_stride < N^d, overflow).
+ * The plan grows a device workspace on first use of a batch size (3D: ~3 × 16 B
+ * per node per cell pair plus a 256 MiB FFT batch; 2D: <= 512 MiB of per-pair
+ * partials); DVM_E_NOMEM if it cannot. */
 DVM_API dvm_status_t dvm_collide_batched(dvm_plan_t plan, const double *f, double *Q, int64_t ncells,
                                  int64_t cell_stride);
 

@@ -551,7 +551,7 @@ dvm_status_t dvm_profile_enable(dvm_plan_t P, int enable)
 }
 
 static const char *kClassNames[] = {"k_linesum", "k_rowsum", "k_reduce", "k_zero", "k_moments", "k_axpy", "plan",
-                                    "k_gain3d", "k_fft", "k_fgain3d"};
+                                    "k_gain3d", "k_fft", "k_fg2", "k_small2d", "k_wline2d", "k_pair2d"};
 
 const char *dvm_profile_name(int k) { return (k >= 0 && k < KC_COUNT) ? kClassNames[k] : nullptr; }
 

@@ -93,7 +93,8 @@ struct Workspace {
 }  // namespace dvm
 
 namespace dvm {
-enum KernelClass { KC_LINESUM = 0, KC_ROWSUM, KC_REDUCE, KC_ZERO, KC_MOMENTS, KC_AXPY, KC_PLAN, KC_GAIN3D, KC_FFT, KC_FGAIN3D, KC_COUNT };
+enum KernelClass { KC_LINESUM = 0, KC_ROWSUM, KC_REDUCE, KC_ZERO, KC_MOMENTS, KC_AXPY, KC_PLAN, KC_GAIN3D, KC_FFT, KC_FGAIN3D,
+                   KC_SMALL2D, KC_WLINE2D, KC_PAIR2D, KC_COUNT };
 struct ProfRec {
     int cls;
     cudaEvent_t a, b;

@@ -290,7 +290,7 @@ dvm_status_t collide_small2d(dvm_plan_s *P, const double *f, int64_t f_stride, d
         // node slices per unit so that one wave covers the SMs (the widest windows dominate)
         const int nslice = (int)std::max<int64_t>(1, std::min<int64_t>(8, sms / ((int64_t)nunits * nc)));
         {
-            LaunchScope ls(P, KC_ROWSUM);
+            LaunchScope ls(P, KC_SMALL2D);
             k_small2d<<<dim3(nunits * nslice, nc), kST, smem, P->stream>>>(f + c0 * f_stride, f_stride, units,
                                                                            nunits, nslice, p, w.p2_part);
         }
@@ -393,13 +393,13 @@ dvm_status_t collide_pair2d(dvm_plan_s *P, const double *f, int64_t f_stride, do
         const int nc = (int)std::min<int64_t>(chunk, ncells - c0);
         dim3 grid((items + kPT - 1) / kPT, nunits, nc);
         {
-            LaunchScope ls(P, KC_LINESUM);
+            LaunchScope ls(P, KC_WLINE2D);
             k_wline2d<<<grid, kPT, 0, P->stream>>>(f + c0 * f_stride, f_stride, nc,
                                                    reinterpret_cast<const Unit2D *>(P->g.units), p, N, P->pk.H,
                                                    w.p2_scr);
         }
         {
-            LaunchScope ls(P, KC_ROWSUM);
+            LaunchScope ls(P, KC_PAIR2D);
             k_pair2d<<<grid, kPT, 0, P->stream>>>(f + c0 * f_stride, f_stride, nc,
                                                   reinterpret_cast<const Unit2D *>(P->g.units), p, N, P->pk.H,
                                                   w.p2_scr, w.p2_part);

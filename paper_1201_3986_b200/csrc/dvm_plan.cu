@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <string>
 #include <vector>
 #include <numeric>
 
@@ -363,6 +364,52 @@ dvm_status_t build_table(dvm_plan_s *P)
         set_error("direction generation produced an invalid count");
         return DVM_E_CUDA;
     }
+    // Plan-time self-check of the table size against closed forms that share
+    // nothing with k_dirgen: 2D A = 4 Σ_{q<=N̄} φ(q); any d,
+    // by Möbius inversion over the gcd, #{e primitive, |e|_inf <= N̄} =
+    // Σ_k μ(k) ((2⌊N̄/k⌋+1)^d − 1), and A is half of it (one of ±e).
+    {
+        auto mu = [](int k) {
+            int r = 1;
+            for (int q = 2; q * q <= k; ++q)
+                if (k % q == 0) {
+                    k /= q;
+                    if (k % q == 0) return 0;
+                    r = -r;
+                }
+            return k > 1 ? -r : r;
+        };
+        long long prim = 0;
+        for (int k = 1; k <= Nb; ++k) {
+            long long side = 2 * (Nb / k) + 1, pw = 1;
+            for (int j = 0; j < d; ++j) pw *= side;
+            prim += mu(k) * (pw - 1);
+        }
+        long long want = prim / 2;
+        if (d == 2) {
+            long long phis = 0;
+            for (int q = 1; q <= Nb; ++q) {
+                int ph = 0;
+                for (int a = 1; a <= q; ++a) {
+                    int x = a, y = q;
+                    while (y) {
+                        const int r = x % y;
+                        x = y;
+                        y = r;
+                    }
+                    ph += x == 1;
+                }
+                phis += ph;
+            }
+            if (4 * phis != want) want = -1;  // the two closed forms disagree: flag below
+            else want = 4 * phis;
+        }
+        if (A != want) {
+            set_error("direction table self-check failed: A = " + std::to_string(A) + ", closed form " +
+                      std::to_string(want));
+            return DVM_E_STATE;
+        }
+    }
     P->A = A;
     P->t.e = d_e;
     DirTable &t = P->t;
@@ -423,6 +470,43 @@ dvm_status_t build_table(dvm_plan_s *P)
     P->local.clear();
     if (P->shard_world <= 1) {
         for (int i = 0; i < A; ++i) P->is_local[i] = 1;
+    } else if (d == 2) {
+        // 2D: shard whole pair units {e, e⊥} (both members share M_e and a_e; the
+        // pair kernels evaluate a unit together, so splitting one would evaluate
+        // it twice).  Unit i < mate[i], in order of its first member; cost per
+        // unit: the pair kernels' per-node work is O(1) per unit (sliding
+        // windows) plus an O(M_e) prologue per line segment -> 64 + 2 M_e + 1.
+        // LPT over the units, ties to the lowest rank, stable.  Mirrored by
+        // paper_1201_3986_b200.parallel.pair_units_2d / lpt_assign.
+        std::vector<int> mate(A, -1);
+        for (int i = 0; i < A; ++i) {
+            int a = -P->h_e[3 * i + 1], b = P->h_e[3 * i];
+            if (a < 0 || (a == 0 && b < 0)) {
+                a = -a;
+                b = -b;
+            }
+            for (int k = 0; k < A; ++k)
+                if (P->h_e[3 * k] == a && P->h_e[3 * k + 1] == b) mate[i] = k;
+            if (mate[i] < 0) {
+                set_error("2D direction table is not closed under e -> e^perp");
+                return DVM_E_STATE;
+            }
+        }
+        std::vector<int> unit_first;
+        for (int i = 0; i < A; ++i)
+            if (i < mate[i]) unit_first.push_back(i);
+        const int U = (int)unit_first.size();
+        std::vector<long long> ucost(U);
+        for (int u = 0; u < U; ++u) ucost[u] = 64 + 2LL * P->h_M[unit_first[u]] + 1;
+        std::vector<int> order(U);
+        std::iota(order.begin(), order.end(), 0);
+        std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return ucost[x] > ucost[y]; });
+        std::vector<long long> load(P->shard_world, 0);
+        for (int u : order) {
+            int r = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+            load[r] += ucost[u];
+            if (r == P->shard_rank) P->is_local[unit_first[u]] = P->is_local[mate[unit_first[u]]] = 1;
+        }
     } else {
         std::vector<int> order(A);
         std::iota(order.begin(), order.end(), 0);

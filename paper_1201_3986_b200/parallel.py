@@ -4,8 +4,9 @@ Two shardings of the hot path (the decomposition eq:decD is
 a sum over directions and the operator is local in x, so both are exact):
 
 * direction sharding of ONE grid (c1-c4): rank r evaluates the LPT share of
-  the directions (libdvm's dvm_plan_ex shard_rank/shard_world) into a partial
-  Q_r, then one fp64 sum all-reduce over NVLink (NCCL) gives Q = sum_r Q_r;
+  the directions (libdvm's dvm_plan_ex shard_rank/shard_world; in 2D whole
+  pair units {e, e⊥}) into a partial Q_r, then one fp64 sum all-reduce over
+  NVLink (NCCL) gives Q = sum_r Q_r;
 * cell sharding of a batch (c5): contiguous blocks of cells per rank, no
   collective on the data path.
 
@@ -40,6 +41,36 @@ def lpt_assign(costs: Sequence[int], world: int) -> np.ndarray:
         r = int(np.argmin(load))
         load[r] += costs[i]
         owner[i] = r
+    return owner
+
+
+def pair_units_2d(dirs: np.ndarray, M: Sequence[int]):
+    """2D pair units {e, e⊥} of a direction table (e⊥ is again
+    a direction of the table, with the same M_e): list of (i, mate) with
+    i < mate in order of i, and the unit costs 64 + 2 M_e + 1 (the pair
+    kernels' O(1) per-node work plus the O(M_e) segment prologue).  Mirrors
+    libdvm's build_table for d = 2."""
+    dirs = np.asarray(dirs)
+    index = {tuple(int(c) for c in e): i for i, e in enumerate(dirs)}
+    units, costs = [], []
+    for i, (a, b) in enumerate(dirs):
+        p = (-int(b), int(a))
+        if p[0] < 0 or (p[0] == 0 and p[1] < 0):
+            p = (-p[0], -p[1])
+        k = index[p]
+        if i < k:
+            units.append((i, k))
+            costs.append(64 + 2 * int(M[i]) + 1)
+    return units, np.asarray(costs, dtype=np.int64)
+
+
+def owners_2d(dirs: np.ndarray, M: Sequence[int], world: int) -> np.ndarray:
+    """Owner rank of every 2D direction: LPT over whole pair units."""
+    units, costs = pair_units_2d(dirs, M)
+    uown = lpt_assign(costs, world)
+    owner = np.full(len(dirs), -1, dtype=np.int64)
+    for (i, k), r in zip(units, uown):
+        owner[i] = owner[k] = r
     return owner
 
 

@@ -115,6 +115,21 @@ def test_lpt_sharding_matches_host_logic():
             assert np.array_equal(loc, owner == r)
 
 
+@pytest.mark.parametrize("name", ["c1", "c3"])
+def test_2d_shards_are_pair_units_matching_host_logic(name):
+    """2D direction sharding assigns whole pair units {e, e⊥},
+    exactly as paper_1201_3986_b200.parallel.owners_2d mirrors it."""
+    from paper_1201_3986_b200 import parallel
+    cfg = dvm_inputs.CONFIGS[name]
+    full = _plan(2, cfg.N, cfg.Nbar)
+    dirs, M, _, _ = full.directions()
+    for world in (2, 3, 8):
+        owner = parallel.owners_2d(dirs, M, world)
+        for r in range(world):
+            loc = _plan(2, cfg.N, cfg.Nbar, shard_rank=r, shard_world=world).directions()[3]
+            assert np.array_equal(loc, owner == r), (world, r)
+
+
 # ---------------------------------------------------------------- parity, full grids
 @pytest.mark.parametrize("name", ["c1", "c2"])
 def test_parity_full_2d(name):

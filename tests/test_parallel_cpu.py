@@ -27,6 +27,25 @@ def _free_port():
     return port
 
 
+def _points(name):
+    cfg = dvm_inputs.CONFIGS[name]
+    nodes = cfg.N ** cfg.d
+    return None if nodes <= 4096 else np.arange(0, nodes, nodes // 997)
+
+
+def _owners(name, world):
+    """The shard sets: 2D whole pair units {e, e⊥} exactly as libdvm assigns
+    them (parallel.owners_2d); 3D a stand-in LPT cost (libdvm's 3D cost needs the
+    plan's perp rows; tests/test_gpu_parity.py checks that mirror on the GPU)."""
+    cfg = dvm_inputs.CONFIGS[name]
+    Nt = oracle.ntilde_rule(cfg.N, cfg.Nbar)
+    dirs = oracle.directions(cfg.d, cfg.Nbar)
+    M = Nt // np.abs(dirs).max(axis=1)
+    if cfg.d == 2:
+        return dirs, parallel.owners_2d(dirs, M, world)
+    return dirs, parallel.lpt_assign(M + 1, world)
+
+
 def _worker(rank, world, port, name, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -35,13 +54,13 @@ def _worker(rank, world, port, name, q):
         cfg = dvm_inputs.CONFIGS[name]
         f = dvm_inputs.make(name)
         Nt = oracle.ntilde_rule(cfg.N, cfg.Nbar)
-        dirs = oracle.directions(cfg.d, cfg.Nbar)
-        costs = [int(Nt // np.abs(e).max()) + 1 for e in dirs]  # any positive cost model
-        owner = parallel.lpt_assign(costs, world)
+        dirs, owner = _owners(name, world)
         mine = dirs[owner == rank]
+        pts = _points(name)
 
         def partial(x):
-            Qp, _, _ = oracle.collide(x, cfg.d, cfg.N, cfg.Nbar, Nt, cfg.L, dirs=mine)
+            Qp, _, _ = oracle.collide(x, cfg.d, cfg.N, cfg.Nbar, Nt, cfg.L, points=pts, dirs=mine,
+                                      nthreads=max(1, (os.cpu_count() or 2) // world), diagnostics=False)
             return torch.from_numpy(Qp)
 
         Q = parallel.sharded_collide(partial, f)
@@ -55,7 +74,7 @@ def _worker(rank, world, port, name, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name", ["c1"])
+@pytest.mark.parametrize("name", ["c1", "c3", "c4"])
 def test_direction_sharded_allreduce_gloo(name):
     world = 2
     ctx = mp.get_context("spawn")
@@ -70,11 +89,30 @@ def test_direction_sharded_allreduce_gloo(name):
         assert p.exitcode == 0
     cfg = dvm_inputs.CONFIGS[name]
     Nt = oracle.ntilde_rule(cfg.N, cfg.Nbar)
-    Qfull, _, _ = oracle.collide(dvm_inputs.make(name), cfg.d, cfg.N, cfg.Nbar, Nt, cfg.L)
+    Qfull, _, _ = oracle.collide(dvm_inputs.make(name), cfg.d, cfg.N, cfg.Nbar, Nt, cfg.L, points=_points(name),
+                                 diagnostics=False)
     np.testing.assert_allclose(Q, Qfull, rtol=0, atol=1e-13 * np.abs(Qfull).max())
     assert 0 < nmine < len(oracle.directions(cfg.d, cfg.Nbar))
     covered = sorted(c for f0, n in ranges for c in range(f0, f0 + n))
     assert covered == list(range(13))
+
+
+@pytest.mark.parametrize("name,units", [("c1", 12), ("c2", 44), ("c3", 160)])
+def test_2d_pair_units_never_split(name, units):
+    """2D shards are whole pair units {e, e⊥} (no unit evaluated twice), every
+    direction owned once, and the unit counts balanced (c3: <= ceil(160/G)+1)."""
+    for world in (2, 4, 8):
+        dirs, owner = _owners(name, world)
+        u, costs = parallel.pair_units_2d(dirs, oracle.ntilde_rule(dvm_inputs.CONFIGS[name].N,
+                                                                  dvm_inputs.CONFIGS[name].Nbar)
+                                          // np.abs(dirs).max(axis=1))
+        assert len(u) == units == len(dirs) // 2
+        assert np.all(owner >= 0)
+        for i, k in u:
+            assert owner[i] == owner[k]
+        per_rank = np.bincount([owner[i] for i, _ in u], minlength=world)
+        assert per_rank.sum() == units
+        assert per_rank.max() <= -(-units // world) + 1
 
 
 def test_lpt_assign_properties():
