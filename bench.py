@@ -219,7 +219,7 @@ BINDING = {
 }
 
 
-def _roofline(prof, psteps, bytes_per_eval, evals_per_step, peak_override=None):
+def _roofline(prof, psteps, bytes_per_eval, evals_per_step, cells=None):
     """roofline object for the dominant kernel: algorithmic (streaming-
     formulation) bytes of the evaluations one launch covers / its CUDA-event
     launch time, against the measured HBM copy bandwidth."""
@@ -231,7 +231,9 @@ def _roofline(prof, psteps, bytes_per_eval, evals_per_step, peak_override=None):
     peak, peak_src = _peaks()
     achieved = alg_bytes / avg_launch_s / 1e9
     km = _kernel_metrics(top_name) or {}
-    traffic = km.get("dram_bytes_per_launch") if km.get("launch_bytes_match", True) else None
+    if km and km.get("cells") is not None and km.get("cells") != cells:
+        km = {}  # the ncu capture was of another launch size: not this launch's counters
+    traffic = km.get("dram_bytes_per_launch")
     r = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
          "traffic": traffic, "kernel": top_name, "kernel_share_of_step": top_ms / total,
          "kernel_avg_launch_ms": top_ms / top_n, "algorithmic_bytes_per_launch": alg_bytes,
@@ -315,7 +317,7 @@ def run_ours(args):
         plan.collide(f, Q)
     prof = plan.profile_read()
     plan.profile(False)
-    roofline = _roofline(prof, psteps, (A + 2) * 8.0 * nodes, cells)
+    roofline = _roofline(prof, psteps, (A + 2) * 8.0 * nodes, cells, cells=cells)
     eff_step_gbs = value / world * (A + 2) * 8.0 * nodes / 1e9
 
     # ---- e2e through the C ABI with host buffers (pinned), copies inside the timed region
@@ -425,13 +427,18 @@ def run_grid(args):
         ms = float(t.item())
     value = (world if c2 else 1) * evals * 1e3 / ms
     A = plan.A
+    # per-launch events inside libdvm; c2's Euler steps 2..100 replay a CUDA graph
+    # (no per-launch events), so its roofline is taken on profiled evaluations
     plan.profile(True)
     psteps = 2
     for _ in range(psteps):
-        step()
+        if c2:
+            plan.collide(f, q)
+        else:
+            step()
     prof = plan.profile_read()
     plan.profile(False)
-    roofline = _roofline(prof, psteps, (A + 2) * 8.0 * nodes, evals)
+    roofline = _roofline(prof, psteps, (A + 2) * 8.0 * nodes, 1, cells=1)
     # e2e with host buffers through the C ABI: f in, Q (and for c2 the final f) out
     fh = torch.from_numpy(f0.copy()).pin_memory()
     qh = torch.empty_like(fh).pin_memory()

@@ -227,6 +227,7 @@ dvm_status_t dvm_plan_info(dvm_plan_t P, dvm_plan_info_t *info)
     bytes += sizeof(double) * (w.p2_scr_elems + w.p2_part_elems);
     bytes += sizeof(double) * (size_t)nd * ((w.qtmp ? 1 : 0) + (w.f1tmp ? 1 : 0));
     bytes += sizeof(double) * (kMaxD + 2) * w.mom_rows;
+    bytes += sizeof(double2) * w.f32_z_elems + sizeof(double) * w.f32_part_elems;
     bytes += sizeof(double) * (w.lv_f_elems + w.lv_q_elems) + sizeof(int64_t) * w.lv_idx_elems +
              sizeof(int) * w.lv_cnt_elems;
     info->workspace_bytes = bytes;
@@ -551,7 +552,7 @@ dvm_status_t dvm_profile_enable(dvm_plan_t P, int enable)
 }
 
 static const char *kClassNames[] = {"k_linesum", "k_rowsum", "k_reduce", "k_zero", "k_moments", "k_axpy", "plan",
-                                    "k_gain3d", "k_fft", "k_fg2", "k_small2d", "k_wline2d", "k_pair2d"};
+                                    "k_gain3d", "k_fft", "k_fg2", "k_small2d", "k_wline2d", "k_pair2d", "k_fg32"};
 
 const char *dvm_profile_name(int k) { return (k >= 0 && k < KC_COUNT) ? kClassNames[k] : nullptr; }
 
@@ -582,9 +583,9 @@ dvm_status_t dvm_set_path(dvm_plan_t P, int path)
         set_error("NULL argument");
         return DVM_E_NULL;
     }
-    if (path < 0 || path > 5) {
+    if (path < 0 || path > 6) {
         set_error("path must be 0 (auto), 1 (v1 orbit sweeps), 2 (gain3d / pair2d), 3 (spectral reference), 4 "
-                  "(3D FFT gain) or 5 (2D small grids)");
+                  "(3D FFT gain), 5 (2D small grids) or 6 (3D N = 32 spectral direction pairs)");
         return DVM_E_STATE;
     }
     P->path_mode = path;

@@ -398,6 +398,11 @@ dvm_status_t reduce_slots(dvm_plan_s *P, double *Q, int64_t q_stride, const doub
     return DVM_OK;
 }
 
+#ifndef FG32_AUTO_CELLS
+#define FG32_AUTO_CELLS 1
+#endif
+constexpr int64_t kFg32AutoCells = FG32_AUTO_CELLS;
+
 dvm_status_t collide_batched(dvm_plan_s *P, const double *f, double *Q, int64_t ncells, int64_t stride)
 {
     const Geo g = geo_of(P);
@@ -407,7 +412,7 @@ dvm_status_t collide_batched(dvm_plan_s *P, const double *f, double *Q, int64_t 
     // N = 256 and at N = 128 with >= 100 directions of this plan's shard, the
     // v1 sweeps otherwise (fewer, latency-bound launches)
     if (P->wt.on) {  // caller weights a(k) b(l): the spectral path evaluates them
-        if (P->path_mode == 1 || P->path_mode == 2 || P->path_mode == 4) {
+        if (P->path_mode == 1 || P->path_mode == 2 || P->path_mode == 4 || P->path_mode == 6) {
             set_error("custom weights (dvm_set_weights) are evaluated by the spectral path: dvm_set_path 0 or 3");
             return DVM_E_STATE;
         }
@@ -418,6 +423,13 @@ dvm_status_t collide_batched(dvm_plan_s *P, const double *f, double *Q, int64_t 
     if (P->path_mode == 4 || (P->path_mode == 0 && P->d == 3 && P->N == 64)) {
         bool handled = false;
         dvm_status_t st = collide_fgain3d(P, f, stride, Q, stride, ncells, &handled);
+        if (st || handled) return st;
+    }
+    // 3D N = 32 (c4): direction pairs through one batched spectral filter (dvm_fg32.cu);
+    // auto for single cells, batches go to the frame-plane kernel (two cells per node)
+    if (P->path_mode == 6 || (P->path_mode == 0 && P->d == 3 && P->N == 32 && ncells <= kFg32AutoCells)) {
+        bool handled = false;
+        dvm_status_t st = collide_fg32(P, f, stride, Q, stride, ncells, &handled);
         if (st || handled) return st;
     }
     // auto for 2D N <= 64: pair units with the loss per pair, f in shared memory (two launches)
@@ -621,7 +633,7 @@ void free_workspace(dvm_plan_s *P)
 {
     clear_profile(P);
     Workspace &w = P->ws;
-    void *ptrs[] = {w.S, w.part, w.f_stage, w.q_stage, w.mom_partial, w.mom_dev, w.qtmp, w.f1tmp, w.mom_ctr, w.fft_z, w.g3_f, w.g3_t, w.g3_q, w.g3_ctr, w.p2_scr, w.p2_part, w.sp_z, w.fg_fhat, w.lv_f, w.lv_q, w.lv_idx, w.lv_cnt};
+    void *ptrs[] = {w.S, w.part, w.f_stage, w.q_stage, w.mom_partial, w.mom_dev, w.qtmp, w.f1tmp, w.mom_ctr, w.fft_z, w.g3_f, w.g3_t, w.g3_q, w.g3_ctr, w.p2_scr, w.p2_part, w.sp_z, w.fg_fhat, w.lv_f, w.lv_q, w.lv_idx, w.lv_cnt, w.f32_z, w.f32_part};
     for (void *q : ptrs)
         if (q) cudaFree(q);
     w = Workspace{};

@@ -624,7 +624,8 @@ dvm_status_t build_gain3d(dvm_plan_s *P)
 void free_gain3d(dvm_plan_s *P)
 {
     GainTables &g = P->g;
-    void *ptrs[] = {g.rec, g.aw, g.tw, g.lamhat, g.units, g.shat, g.that, g.fg_rec, g.fg_aw, g.fg_t2d};
+    void *ptrs[] = {g.rec, g.aw, g.tw, g.lamhat, g.units, g.shat, g.that, g.fg_rec, g.fg_aw, g.fg_t2d,
+                    g.f32_rec, g.f32_off, g.f32_aw, g.f32_t2d};
     for (void *q : ptrs)
         if (q) cudaFree(q);
     g = GainTables{};

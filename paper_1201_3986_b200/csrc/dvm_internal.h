@@ -82,6 +82,9 @@ struct Workspace {
     size_t p2_scr_elems = 0, p2_part_elems = 0;
     double2 *sp_z = nullptr;        // spectral path: f̂ and the per-direction transform
     size_t sp_z_elems = 0;
+    double2 *f32_z = nullptr;       // N = 32 spectral gain: one complex array per direction pair
+    double *f32_part = nullptr;     // N = 32 spectral gain: per-chunk partial gains
+    size_t f32_z_elems = 0, f32_part_elems = 0;
     double2 *fg_fhat = nullptr;     // FFT gain: f̂ of the cell pairs [pairs][nodes]
     size_t fg_fhat_elems = 0;
     double *lv_f = nullptr, *lv_q = nullptr;  // per-cell N̄: gathered cells of one level and their Q
@@ -94,7 +97,7 @@ struct Workspace {
 
 namespace dvm {
 enum KernelClass { KC_LINESUM = 0, KC_ROWSUM, KC_REDUCE, KC_ZERO, KC_MOMENTS, KC_AXPY, KC_PLAN, KC_GAIN3D, KC_FFT, KC_FGAIN3D,
-                   KC_SMALL2D, KC_WLINE2D, KC_PAIR2D, KC_COUNT };
+                   KC_SMALL2D, KC_WLINE2D, KC_PAIR2D, KC_FG32, KC_COUNT };
 struct ProfRec {
     int cls;
     cudaEvent_t a, b;
@@ -118,6 +121,11 @@ struct GainTables {
     int4 *fg_rec = nullptr;   // FFT gain: [A_local][3] (e, M), (u, 0), (w, 0)
     double *fg_aw = nullptr;  // FFT gain: [A_local] a_e / N^3
     double *fg_t2d = nullptr; // FFT gain: [A_local][N][N] plane-filter spectra T2D_e(p, q)
+    int4 *f32_rec = nullptr;  // N = 32 spectral gain: [A_local] (u, M), [A_local] (w, 0) (see dvm_fg32.cu)
+    uint32_t *f32_off = nullptr; // N = 32 spectral gain: [A_local][2 M_max] packed tap offsets ±m e
+    double *f32_aw = nullptr; // N = 32 spectral gain: [A_local] a_e / N^3
+    double *f32_t2d = nullptr; // N = 32 spectral gain: [A_local][N][N]
+    int f32_mmax = 0;
     size_t bytes = 0;
 };
 
@@ -255,6 +263,7 @@ dvm_status_t build_loss(dvm_plan_s *P);
 dvm_status_t set_weights(dvm_plan_s *P, const double *a_box, const double *b_box);
 void free_weights(dvm_plan_s *P);
 dvm_status_t fft_forward_pairs(dvm_plan_s *P, const double *f, int64_t f_stride, int64_t ncells, double2 *out);
+dvm_status_t ifft_batch(dvm_plan_s *P, double2 *z, int64_t narrays);
 dvm_status_t loss_init(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q, int64_t q_stride, int64_t ncells,
                        double2 *QI);
 dvm_status_t collide_spectral(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q, int64_t q_stride,
@@ -275,6 +284,9 @@ dvm_status_t collide_fgain3d(dvm_plan_s *P, const double *f, int64_t f_stride, d
                              int64_t ncells, bool *handled);
 dvm_status_t collide_gain3d(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q, int64_t q_stride,
                             int64_t ncells, bool *handled);
+// 3D N = 32 gain by batched direction-pair spectral filtering (dvm_fg32.cu)
+dvm_status_t collide_fg32(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q, int64_t q_stride,
+                          int64_t ncells, bool *handled);
 void free_workspace(dvm_plan_s *P);
 
 }  // namespace dvm

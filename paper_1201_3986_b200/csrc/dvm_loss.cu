@@ -562,6 +562,25 @@ dvm_status_t set_weights(dvm_plan_s *P, const double *a_box, const double *b_box
 
 // f̂ of cell pairs: out[p] = FFT_d(f_{2p} + i f_{2p+1}) (forward, unnormalised;
 // an odd tail cell is paired with zero).
+// d unnormalised inverse passes, in place, over `narrays` complex N^d arrays
+dvm_status_t ifft_batch(dvm_plan_s *P, double2 *z, int64_t narrays)
+{
+    const int d = P->d;
+    for (int k = 0; k < d; ++k) {
+        FftArgs a = {};
+        a.d = d;
+        a.npairs = narrays;
+        a.tw = P->g.tw;
+        a.inverse = 1;
+        a.ax = k;
+        a.zin = z;
+        a.zout = z;
+        dvm_status_t st = fft_dispatch(P, a);
+        if (st) return st;
+    }
+    return DVM_OK;
+}
+
 dvm_status_t fft_forward_pairs(dvm_plan_s *P, const double *f, int64_t f_stride, int64_t ncells, double2 *out)
 {
     const int d = P->d;

@@ -666,3 +666,78 @@ def test_weighted_errors_and_reset():
     p.set_weights(None, None)
     p.set_path(0)
     np.testing.assert_array_equal(_gpu(p, f), q_default)
+
+
+# ---------------------------------------------------------------- BKW accuracy workload
+def test_bkw_rk2_matches_oracle_heun():
+    """The BKW workload's stepping (dvm_rk2 on the operator with the Carleman
+    weights a(k) = h^2/(π gcd k), reading R24) on a c1-sized grid (N = 16, box
+    T = 5.5, N̄ = Ñ = 3) equals the same TVD-RK2 (Heun) evaluated with the CPU
+    oracle and the same weight table, for 3 steps."""
+    from paper_1201_3986_b200 import bkw
+    N, T, Nbar, dt, steps = 16, 5.5, 3, 0.01, 3
+    p = bkw.make_plan(N, Nbar, T)
+    a_box = bkw.carleman_weights(p.Ntilde, p.h)
+    v2 = bkw.grid_v2(N, T)
+    f0 = bkw.f_exact(0.0, v2).reshape(-1)
+    f = torch.from_numpy(f0.copy()).cuda()
+    p.rk2(f, dt, steps)
+    fo = f0.copy()
+    for _ in range(steps):
+        q0 = oracle.collide(fo, 2, N, Nbar, p.Ntilde, T, a_box=a_box)[0].reshape(-1)
+        f1 = fo + dt * q0
+        q1 = oracle.collide(f1, 2, N, Nbar, p.Ntilde, T, a_box=a_box)[0].reshape(-1)
+        fo = 0.5 * (fo + (f1 + dt * q1))
+    assert np.abs(f.cpu().numpy() - fo).max() <= 1e-13 * np.abs(fo).max()
+
+
+def test_bkw_carleman_weights_are_the_bkw_operator():
+    """Reading R24: with a(k) = h^2/(π gcd k) the operator converges to the
+    exact BKW time derivative (L1 residual of the best constant fit -> 0 with N,
+    best constant -> ~1.08, the |x|,|y| <= Ñh truncation), while the printed
+    h^3|k|/gcd k does not (a residual near 20 % at every N)."""
+    from paper_1201_3986_b200 import bkw
+    res = {}
+    for weights in ("carleman", "printed"):
+        for N in (16, 32, 64):
+            T = bkw.PAPER_BOX[N]
+            p = bkw.make_plan(N, _plan(2, N, 1, L=T).Ntilde, T, weights)
+            v2 = bkw.grid_v2(N, T)
+            q = p.collide(torch.from_numpy(bkw.f_exact(0.0, v2).reshape(-1)).cuda()).cpu().numpy()
+            ft = bkw.dfdt_exact(0.0, v2).reshape(-1)
+            c = float(np.dot(q, ft) / np.dot(q, q))
+            res[weights, N] = (c, np.abs(c * q - ft).sum() / np.abs(ft).sum())
+    assert res["carleman", 16][1] > res["carleman", 32][1] > res["carleman", 64][1]
+    assert res["carleman", 64][1] < 0.02 and 1.0 < res["carleman", 64][0] < 1.15
+    assert all(res["printed", N][1] > 0.15 for N in (16, 32, 64))
+
+
+def test_bkw_e1_decreases_with_N():
+    """Table 1's trend: with the physical operator (c = 1) the
+    relative L1 error after one RK2 step of dt = 0.01 from the BKW datum
+    decreases as the grid is refined (paper's boxes, all lines N̄ = Ñ)."""
+    from paper_1201_3986_b200 import bkw
+    errs = []
+    for N in (16, 32, 64):
+        Nt = _plan(2, N, 1, L=bkw.PAPER_BOX[N]).Ntilde
+        errs.append(bkw.run(N, Nt)[0])
+    assert errs[0] > errs[1] > errs[2] > 0, errs
+
+
+# ---------------------------------------------------------------- 3D N = 32 direction-pair spectral gain (path 6)
+@pytest.mark.parametrize("Nbar,Nt,cells,shard", [(4, 7, 1, None), (2, 5, 3, None), (4, 7, 1, (1, 3)), (1, 3, 2, None)])
+def test_fg32_path_matches_oracle(Nbar, Nt, cells, shard):
+    """dvm_set_path(6): T_a + i T_b = IFFT(f̂ (t̂_a + i t̂_b)) for direction pairs of
+    one real cell (reading R23), taps for S_e, partials in chunk order: every
+    node against the oracle (c4 geometry), odd direction counts (a lone last
+    direction), several cells and a direction shard."""
+    f = np.stack([dvm_inputs.two_bumps(3, 32, 8.0, 1.0 + 0.25 * c, 0.01, 40 + c).reshape(-1) for c in range(cells)])
+    kw = {} if shard is None else {"shard_rank": shard[0], "shard_world": shard[1]}
+    p = _plan(3, 32, Nbar, Ntilde=Nt, **kw)
+    p.set_path(6)
+    q6 = _gpu(p, f)
+    assert np.array_equal(q6, _gpu(p, f))  # bitwise repeatable
+    dirs = p.directions()[0][p.directions()[3].astype(bool)] if shard else None
+    for c in range(cells):
+        Qo, _, _ = oracle.collide(f[c], 3, 32, Nbar, Nt, 8.0, dirs=dirs, diagnostics=False)
+        _assert_parity(q6[c], Qo[0], f"fg32 N̄={Nbar} Ñ={Nt} cell {c}")
