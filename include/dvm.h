@@ -222,7 +222,10 @@ DVM_API const char *dvm_profile_name(int k);
  * CTA per direction pair {e, e⊥} and cell holds f in shared memory and
  * evaluates gain and loss of the pair with direct line windows (the loss as
  * f [a (Box − W_e⊥) + a (Box − W_e)], Box the 2D window), partials summed in
- * pair order (two launches, no FFT), 3 = the spectral reference
+ * pair order (two launches, no FFT), 6 = 3D N = 32: two directions of one
+ * cell per complex transform, T_a + i T_b = IFFT(f̂ (t̂_a + i t̂_b)), all
+ * direction pairs in one batch plus the loss array f̂ λ̂ (auto for batches of
+ * <= 2 cells at N = 32), 3 = the spectral reference
  * path (per direction one inverse transform gives
  * S_e + i T_e from the real filter spectra; a second cross-check, slow:
  * A inverse FFTs per cell; its tables need 16 A N^d bytes, <= 4 GB).  The FFT-loss paths evaluate

@@ -399,7 +399,7 @@ dvm_status_t reduce_slots(dvm_plan_s *P, double *Q, int64_t q_stride, const doub
 }
 
 #ifndef FG32_AUTO_CELLS
-#define FG32_AUTO_CELLS 1
+#define FG32_AUTO_CELLS 2
 #endif
 constexpr int64_t kFg32AutoCells = FG32_AUTO_CELLS;
 

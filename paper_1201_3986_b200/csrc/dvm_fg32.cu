@@ -24,7 +24,7 @@ namespace {
 
 constexpr int K32 = 32;
 constexpr int K32N = K32 * K32 * K32;
-constexpr int K32CHUNKS = 16;  // direction-pair chunks of the gain kernel (partials summed in order)
+constexpr int K32CHUNKS = 32;  // direction-pair chunks of the gain kernel (partials summed in order)
 
 // T2D_e(p, q) = Σ_{(α, β) ∈ P_e} cos(2π(α p + β q) / N), one thread per (direction, p, q)
 __global__ void k_f32_t2d(int nloc, const int *local, const int *row_off, const int *row_b, const int *row_lo,
@@ -43,55 +43,213 @@ __global__ void k_f32_t2d(int nloc, const int *local, const int *row_off, const 
     out[gid] = acc;
 }
 
-// Z[p][ξ] = f̂(ξ) (t̂_{2p}(ξ) + i t̂_{2p+1}(ξ))   (t̂ of a missing partner: 0)
-__global__ void k_f32_mult(const double2 *__restrict__ fhat, const double *__restrict__ t2d,
-                           const int4 *__restrict__ ru, const int4 *__restrict__ rw, int nloc, int npairs,
-                           double2 *__restrict__ Z)
+constexpr int P32 = K32 + 1;  // padded pitch of a 32 x 32 tile in shared memory (double2)
+
+__device__ __forceinline__ double2 cmul32(double2 a, double2 b)
 {
-    const int64_t total = (int64_t)npairs * K32N;
-    for (int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gid < total;
-         gid += (int64_t)gridDim.x * blockDim.x) {
-        const int p = (int)(gid / K32N), x = (int)(gid % K32N);
-        const int x0 = x >> 10, x1 = (x >> 5) & 31, x2 = x & 31;
-        auto filt = [&](int k) {
-            const int4 u = ru[k], w = rw[k];
-            const int pu = (u.x * x0 + u.y * x1 + u.z * x2) & (K32 - 1);
-            const int pw = (w.x * x0 + w.y * x1 + w.z * x2) & (K32 - 1);
-            return t2d[(int64_t)k * K32 * K32 + pu * K32 + pw];
-        };
-        const double ta = filt(2 * p), tb = 2 * p + 1 < nloc ? filt(2 * p + 1) : 0.0;
-        const double2 fh = fhat[x];
-        Z[gid] = make_double2(fh.x * ta - fh.y * tb, fh.x * tb + fh.y * ta);
-    }
+    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 add2_(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 sub2_(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+// inverse-sign DFTs (y_k = Σ_n a_n e^{+2πi nk/n}), natural order in and out
+__device__ __forceinline__ void idft4_(double2 &a0, double2 &a1, double2 &a2, double2 &a3)
+{
+    const double2 t0 = add2_(a0, a2), t1 = sub2_(a0, a2), t2 = add2_(a1, a3), d = sub2_(a1, a3);
+    const double2 t3 = make_double2(-d.y, d.x);
+    a0 = add2_(t0, t2);
+    a2 = sub2_(t0, t2);
+    a1 = add2_(t1, t3);
+    a3 = sub2_(t1, t3);
+}
+__device__ __forceinline__ void idft8_(double2 (&v)[8])
+{
+    double2 e0 = v[0], e1 = v[2], e2 = v[4], e3 = v[6], o0 = v[1], o1 = v[3], o2 = v[5], o3 = v[7];
+    idft4_(e0, e1, e2, e3);
+    idft4_(o0, o1, o2, o3);
+    constexpr double c = 0.70710678118654752440;
+    o1 = make_double2(c * (o1.x - o1.y), c * (o1.x + o1.y));
+    o2 = make_double2(-o2.y, o2.x);
+    o3 = make_double2(-c * (o3.x + o3.y), c * (o3.x - o3.y));
+    v[0] = add2_(e0, o0);
+    v[4] = sub2_(e0, o0);
+    v[1] = add2_(e1, o1);
+    v[5] = sub2_(e1, o1);
+    v[2] = add2_(e2, o2);
+    v[6] = sub2_(e2, o2);
+    v[3] = add2_(e3, o3);
+    v[7] = sub2_(e3, o3);
 }
 
-// part[chunk][x] = Σ_{pairs of the chunk, in order} a_a S_a(x) T_a(x) + a_b S_b(x) T_b(x)
-__global__ void __launch_bounds__(256) k_f32_gain(const double *__restrict__ f, const double2 *__restrict__ Z,
-                                                  const uint32_t *__restrict__ off, int mmax2,
-                                                  const int4 *__restrict__ ru, const double *__restrict__ aw,
-                                                  int nloc, int npairs, int ppc, uint32_t H,
-                                                  double *__restrict__ part)
+// Inverse 32-point DFTs of the 32 lines of a 32 x 32 tile in shared memory, in
+// place: element n of line l at buf[l * ls + n * es].  128 threads: thread
+// (l = t >> 2, j = t & 3) takes n = j + 4 q (q < 8): DFT-8 over q -> k1,
+// × ω32^{j k1}, then DFT-4 over j for k1 = 2 j', 2 j' + 1 -> k = k1 + 8 k2.
+__device__ __forceinline__ void ifft32_lines(double2 *buf, int ls, int es, const double2 *tw32)
 {
-    const int x = blockIdx.x * blockDim.x + threadIdx.x;
-    const int chunk = blockIdx.y;
-    if (x >= K32N) return;
+    const int t = threadIdx.x, l = t >> 2, j = t & 3;
+    double2 v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = buf[l * ls + (j + 4 * q) * es];
+    idft8_(v);
+#pragma unroll
+    for (int k1 = 1; k1 < 8; ++k1) v[k1] = cmul32(v[k1], tw32[(j * k1) & (K32 - 1)]);
+    __syncthreads();
+#pragma unroll
+    for (int k1 = 0; k1 < 8; ++k1) buf[l * ls + (j + 4 * k1) * es] = v[k1];
+    __syncthreads();
+    double2 a[2][4];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int k1 = 2 * j + h;
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) a[h][jj] = buf[l * ls + (jj + 4 * k1) * es];
+        idft4_(a[h][0], a[h][1], a[h][2], a[h][3]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int k2 = 0; k2 < 4; ++k2) buf[l * ls + (2 * j + h + 8 * k2) * es] = a[h][k2];
+    __syncthreads();
+}
+
+// One CTA per (direction pair p, plane ξ_0): the plane of f̂ (t̂_{2p} + i t̂_{2p+1}),
+// inverse 2D DFT over (ξ_1, ξ_2), written to Z[p][ξ_0][y][z].
+__global__ void __launch_bounds__(128) k_f32_plane(const double2 *__restrict__ fhat, const double *__restrict__ t2d,
+                                                   const int4 *__restrict__ ru, const int4 *__restrict__ rw,
+                                                   int nloc, int npairs, const double *__restrict__ lamhat,
+                                                   double2 *__restrict__ Z)
+{
+    __shared__ double2 buf[K32 * P32];
+    __shared__ double2 tw32[K32];
+    const int p = blockIdx.x / K32, x0 = blockIdx.x % K32;
+    const int t = threadIdx.x;
+    if (t < K32) {
+        double s, c;
+        sincospi(2.0 * t / K32, &s, &c);
+        tw32[t] = make_double2(c, s);
+    }
+    if (p == npairs) {
+        // the loss array: f̂ λ̂ (λ̂ real, the spectrum of the loss kernel λ, reading R21)
+        for (int i = t; i < K32 * K32; i += 128) {
+            const double2 fh = fhat[x0 * K32 * K32 + i];
+            const double l = lamhat[x0 * K32 * K32 + i];
+            buf[(i >> 5) * P32 + (i & 31)] = make_double2(fh.x * l, fh.y * l);
+        }
+        __syncthreads();
+        ifft32_lines(buf, P32, 1, tw32);
+        ifft32_lines(buf, 1, P32, tw32);
+        double2 *dst = Z + ((int64_t)p * K32 + x0) * K32 * K32;
+        for (int i = t; i < K32 * K32; i += 128) dst[i] = buf[(i >> 5) * P32 + (i & 31)];
+        return;
+    }
+    const int ka = 2 * p, kb = 2 * p + 1;
+    const int4 ua = ru[ka], wa = rw[ka];
+    const bool hb = kb < nloc;
+    const int4 ub = hb ? ru[kb] : make_int4(0, 0, 0, 0), wb = hb ? rw[kb] : make_int4(0, 0, 0, 0);
+    const double *Ta = t2d + (int64_t)ka * K32 * K32, *Tb = t2d + (int64_t)(hb ? kb : ka) * K32 * K32;
+    for (int i = t; i < K32 * K32; i += 128) {
+        const int x1 = i >> 5, x2 = i & 31;
+        const double ta = Ta[((ua.x * x0 + ua.y * x1 + ua.z * x2) & 31) * K32 + ((wa.x * x0 + wa.y * x1 + wa.z * x2) & 31)];
+        const double tb = hb ? Tb[((ub.x * x0 + ub.y * x1 + ub.z * x2) & 31) * K32 +
+                                  ((wb.x * x0 + wb.y * x1 + wb.z * x2) & 31)]
+                             : 0.0;
+        const double2 fh = fhat[x0 * K32 * K32 + i];
+        buf[x1 * P32 + x2] = make_double2(fh.x * ta - fh.y * tb, fh.x * tb + fh.y * ta);
+    }
+    __syncthreads();
+    ifft32_lines(buf, P32, 1, tw32);  // along ξ_2 -> z
+    ifft32_lines(buf, 1, P32, tw32);  // along ξ_1 -> y
+    double2 *dst = Z + ((int64_t)p * K32 + x0) * K32 * K32;
+    for (int i = t; i < K32 * K32; i += 128) dst[i] = buf[(i >> 5) * P32 + (i & 31)];
+}
+
+// One CTA per (row y, pair chunk): for every pair of the chunk, the inverse DFT
+// along ξ_0 of Z[p][:][y][:] gives T_a + i T_b on the 32 x 32 nodes (x, y, z);
+// then G += a_a S_a T_a + a_b S_b T_b (S as taps of f), G in registers, written
+// as this chunk's partial.  Thread t owns z = t & 31, x = (t >> 5) + 4 i.
+__global__ void __launch_bounds__(128) k_f32_xgain(const double *__restrict__ f, const double2 *__restrict__ Z,
+                                                   const uint32_t *__restrict__ off, int mmax2,
+                                                   const int4 *__restrict__ ru, const double *__restrict__ aw,
+                                                   int nloc, int npairs, int ppc, uint32_t H,
+                                                   double *__restrict__ part)
+{
+    __shared__ double2 buf[K32 * P32];
+    __shared__ double2 tw32[K32];
+    const int y = blockIdx.x, chunk = blockIdx.y;
+    const int t = threadIdx.x, z = t & 31, xb = t >> 5;
+    if (t < K32) {
+        double s, c;
+        sincospi(2.0 * t / K32, &s, &c);
+        tw32[t] = make_double2(c, s);
+    }
+    double G[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) G[i] = 0.0;
     const int p0 = chunk * ppc, p1 = min(npairs, p0 + ppc);
-    double acc = 0.0;
     for (int p = p0; p < p1; ++p) {
-        const double2 z = Z[(int64_t)p * K32N + x];
+        __syncthreads();
+        const double2 *src = Z + (int64_t)p * K32N + y * K32;
+        for (int i = t; i < K32 * K32; i += 128) buf[(i >> 5) * P32 + (i & 31)] = src[(i >> 5) * K32 * K32 + (i & 31)];
+        __syncthreads();
+        ifft32_lines(buf, 1, P32, tw32);  // along ξ_0 -> x: buf[x][z]
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
             const int k = 2 * p + s;
             if (k >= nloc) break;
             const int m2 = 2 * ru[k].w;
             const uint32_t *o = off + (int64_t)k * mmax2;
-            double S = 0.0;
-            for (int t = 0; t < m2; t += 2)
-                S += __ldg(f + swar_add((uint32_t)x, o[t], H)) + __ldg(f + swar_add((uint32_t)x, o[t + 1], H));
-            acc += aw[k] * (s ? z.y : z.x) * S;
+            const double a = aw[k];
+            double S[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) S[i] = 0.0;
+            const uint32_t n0 = (uint32_t)((xb * K32 + y) * K32 + z);
+            // taps ±m e: 16 independent loads per pair of taps (8 nodes 4 x-planes apart)
+            for (int q = 0; q < m2; q += 2) {
+                const uint32_t b0 = swar_add(n0, o[q], H), b1 = swar_add(n0, o[q + 1], H);
+                double va[8], vb[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    va[i] = __ldg(f + ((b0 + (uint32_t)(4 * i * K32 * K32)) & (uint32_t)(K32N - 1)));
+                    vb[i] = __ldg(f + ((b1 + (uint32_t)(4 * i * K32 * K32)) & (uint32_t)(K32N - 1)));
+                }
+#pragma unroll
+                for (int i = 0; i < 8; ++i) S[i] += va[i] + vb[i];
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const double2 T = buf[(xb + 4 * i) * P32 + z];
+                G[i] += a * (s ? T.y : T.x) * S[i];
+            }
         }
     }
-    part[(int64_t)chunk * K32N + x] = acc;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) part[(int64_t)chunk * K32N + ((xb + 4 * i) * K32 + y) * K32 + z] = G[i];
+}
+
+// One CTA per row y: the loss array's transform along ξ_0 gives N^3 Λ(x, y, z);
+// Q := −f Λ (the loss of eq:decD as one convolution, reading R21).
+__global__ void __launch_bounds__(128) k_f32_xloss(const double *__restrict__ f, const double2 *__restrict__ Zl,
+                                                   double *__restrict__ Q)
+{
+    __shared__ double2 buf[K32 * P32];
+    __shared__ double2 tw32[K32];
+    const int y = blockIdx.x, t = threadIdx.x;
+    if (t < K32) {
+        double s, c;
+        sincospi(2.0 * t / K32, &s, &c);
+        tw32[t] = make_double2(c, s);
+    }
+    const double2 *src = Zl + y * K32;
+    for (int i = t; i < K32 * K32; i += 128) buf[(i >> 5) * P32 + (i & 31)] = src[(i >> 5) * K32 * K32 + (i & 31)];
+    __syncthreads();
+    ifft32_lines(buf, 1, P32, tw32);
+    constexpr double inv = 1.0 / (double)K32N;
+    for (int i = t; i < K32 * K32; i += 128) {
+        const int x = i >> 5, z = i & 31;
+        const int n = (x * K32 + y) * K32 + z;
+        Q[n] = -f[n] * (buf[x * P32 + z].x * inv);
+    }
 }
 
 // Q[x] += Σ_chunk part[chunk][x], chunks in order (Q holds −fΛ)
@@ -165,30 +323,30 @@ dvm_status_t collide_fg32(dvm_plan_s *P, const double *f, int64_t f_stride, doub
     const int nchunks = std::max(1, std::min(K32CHUNKS, npairs));
     const int ppc = npairs > 0 ? (npairs + nchunks - 1) / nchunks : 0;
     Workspace &w = P->ws;
-    if ((st = grow(&w.f32_z, &w.f32_z_elems, (size_t)(std::max(1, npairs) + 1) * K32N, P->stream))) return st;
+    // arrays: npairs direction pairs, the loss array, f̂
+    if ((st = grow(&w.f32_z, &w.f32_z_elems, (size_t)(npairs + 2) * K32N, P->stream))) return st;
     if ((st = grow(&w.f32_part, &w.f32_part_elems, (size_t)nchunks * K32N, P->stream))) return st;
-    // Q := −f Λ for every cell (the loss, one FFT convolution per cell pair)
-    if ((st = loss_init(P, f, f_stride, Q, q_stride, ncells, nullptr))) return st;
-    if (nloc == 0) {
-        *handled = true;
-        return DVM_OK;
-    }
-    double2 *fhat = w.f32_z + (size_t)npairs * K32N;
+    double2 *fhat = w.f32_z + (size_t)(npairs + 1) * K32N;
     const GainTables &g = P->g;
     for (int64_t c = 0; c < ncells; ++c) {
         if ((st = fft_forward_pairs(P, f + c * f_stride, f_stride, 1, fhat))) return st;
         {
             LaunchScope ls(P, KC_FG32);
-            k_f32_mult<<<1184, 256, 0, P->stream>>>(fhat, g.f32_t2d, g.f32_rec, g.f32_rec + nloc, nloc, npairs,
-                                                    w.f32_z);
+            k_f32_plane<<<(npairs + 1) * K32, 128, 0, P->stream>>>(fhat, g.f32_t2d, g.f32_rec, g.f32_rec + nloc,
+                                                                   nloc, npairs, g.lamhat, w.f32_z);
             DVM_CUDA(cudaGetLastError());
         }
-        if ((st = ifft_batch(P, w.f32_z, npairs))) return st;
         {
             LaunchScope ls(P, KC_FG32);
-            k_f32_gain<<<dim3(K32N / 256, nchunks), 256, 0, P->stream>>>(f + c * f_stride, w.f32_z, g.f32_off,
-                                                                         2 * g.f32_mmax, g.f32_rec, g.f32_aw, nloc,
-                                                                         npairs, ppc, P->pk.H, w.f32_part);
+            k_f32_xloss<<<K32, 128, 0, P->stream>>>(f + c * f_stride, w.f32_z + (size_t)npairs * K32N, Q + c * q_stride);
+            DVM_CUDA(cudaGetLastError());
+        }
+        if (nloc == 0) continue;
+        {
+            LaunchScope ls(P, KC_FG32);
+            k_f32_xgain<<<dim3(K32, nchunks), 128, 0, P->stream>>>(f + c * f_stride, w.f32_z, g.f32_off,
+                                                                  2 * g.f32_mmax, g.f32_rec, g.f32_aw, nloc, npairs,
+                                                                  ppc, P->pk.H, w.f32_part);
             DVM_CUDA(cudaGetLastError());
         }
         {
