@@ -42,6 +42,9 @@ constexpr int FMS = 32;          // tap table size (2 M_e <= 32)
 #ifndef FG2_REGA
 #define FG2_REGA 104  // k_fg2 setmaxnreg split: phase A, phase B gets 256 - FG2_REGA
 #endif
+#ifndef FG_BULK
+#define FG_BULK 1  // phase-A plane / T2D loads as one bulk copy each (mbarrier) instead of cp.async
+#endif
 #ifndef FG_TMEM_EARLY
 #define FG_TMEM_EARLY 1  // accumulator TMEM loads issued before the taps (B alone 48.6 -> 46.9 ms / 18 cells)
 #endif
@@ -185,6 +188,37 @@ __device__ __forceinline__ void idft16(double2 (&v)[16])
     for (int k = 0; k < 16; ++k) v[k] = o[k];
 }
 
+__device__ __forceinline__ void mbar_init(uint64_t *m, int count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(m)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *m, uint32_t phase)
+{
+    const uint32_t a = (uint32_t)__cvta_generic_to_shared(m);
+    uint32_t done = 0;
+    while (!done)
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                     : "=r"(done)
+                     : "r"(a), "r"(phase)
+                     : "memory");
+}
+// one thread: expect `bytes` on the barrier, then bulk copies (TMA engine) complete them
+__device__ __forceinline__ void mbar_expect(uint64_t *m, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(m)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *m, uint64_t pol)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            (uint32_t)__cvta_generic_to_shared(dst)),
+        "l"(src), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(m)), "l"(pol)
+        : "memory");
+}
+
 template <int CL>
 __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
 {
@@ -199,6 +233,7 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
     double2 *rb = tw + FN;  // phase-B x-FFT exchange [2][FN][32]
     __shared__ uint32_t soff[2][FMS];
     __shared__ uint32_t s_tmem;
+    __shared__ __align__(8) uint64_t s_mbar;  // FG_BULK: completion of the phase-A bulk loads
 
     const bool roleA = threadIdx.x < kRoleT;
     const int t = threadIdx.x & (kRoleT - 1);
@@ -224,10 +259,27 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
+    if (threadIdx.x == 0) {
+        mbar_init(&s_mbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
+#if FG_BULK
+    // one bulk copy per table: the plane of f̂ (64 KB) and T2D_e (32 KB), issued by
+    // thread 0 of phase A, completing the phase of s_mbar
+    auto issue = [&](const double2 *fh, int g, int di) {
+        if (t == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect(&s_mbar, (uint32_t)(sizeof(double2) * FN2 + (di >= 0 ? sizeof(double) * FN2 : 0)));
+            bulk_g2s(stg, fh + (int64_t)g * FN2, (uint32_t)(sizeof(double2) * FN2), &s_mbar, l2_drop());
+            if (di >= 0) bulk_g2s(t2, A.t2d + (int64_t)di * FN2, (uint32_t)(sizeof(double) * FN2), &s_mbar, l2_keep());
+        }
+    };
+    uint32_t mph = 0;
+#endif
     auto load_t2d = [&](int di) {
         const double2 *src = reinterpret_cast<const double2 *>(A.t2d + (int64_t)di * FN2);
         for (int i = t; i < FN2 / 2; i += kRoleT) cp_async16_pol(t2 + 2 * i, src + i, l2_keep());
@@ -247,9 +299,13 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
         const int sw = c_me & 7;
         const int zr = t & 63, kq1r = t >> 6;  // CTA exchange reader: (z, kq1)
         if (grp < items && !(A.dbg & 2)) {
+#if FG_BULK
+            issue(A.fhat + (grp / A.nchunks) * FNODES, rank, (int)((int64_t)A.nloc * (grp % A.nchunks) / A.nchunks));
+#else
             load_plane(A.fhat + (grp / A.nchunks) * FNODES, rank);
             load_t2d((int)((int64_t)A.nloc * (grp % A.nchunks) / A.nchunks));
             cp_async_commit();
+#endif
         }
         for (int64_t item = grp; item < items; item += ngroups) {
             const int64_t pair = item / A.nchunks;
@@ -274,8 +330,13 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
                 for (int kp = 0; kp < ((A.dbg & 2) ? 0 : FPL); ++kp) {
                     const int g = rank + kp * CL;
                     const bool lastp = kp + 1 == FPL;
+#if FG_BULK
+                    mbar_wait(&s_mbar, mph);  // [1] the plane (and at kp = 0 T2D_e) is in shared memory
+                    mph ^= 1;
+#else
                     cp_async_wait_all();
                     role_sync(bar);  // [1] the plane (and at kp = 0 T2D_e) is in shared memory
+#endif
                     double2 v[16];
                     {
                         // stage 1: f̂ t̂_e, radix-4 over ξ_z high and ξ_y high
@@ -316,6 +377,12 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
                         v[n] = x1w[(c_me >> 2) * 16 * FN + 16 * (c_me & 3) + (n ^ sw)];
                     idft16(v);  // z = kp1 + 4 kp2: v[kp2], kp1 = c_me & 3
                     role_sync(bar);  // [2] staging and the exchange buffer are free
+#if FG_BULK
+                    if (!lastp)
+                        issue(fh, g + CL, -1);
+                    else if (ndi >= 0)
+                        issue(fh_next, rank, ndi);
+#else
                     if (!lastp) {
                         load_plane(fh, g + CL);
                     } else if (ndi >= 0) {
@@ -323,6 +390,7 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
                         load_t2d(ndi);
                     }
                     cp_async_commit();
+#endif
                     {
                         const int kp1 = c_me & 3, kq1 = c_me >> 2;
                         double2 *dst = ex + kq1 * F2Q + yl * FN + kp1;
