@@ -45,6 +45,10 @@ constexpr int FMS = 32;          // tap table size (2 M_e <= 32)
 #ifndef FG_BULK
 #define FG_BULK 1  // phase-A plane / T2D loads as one bulk copy each (mbarrier) instead of cp.async
 #endif
+#ifndef T2D_SWZ
+#define T2D_SWZ 1  // XOR column swizzle of the T2D_e table: fewer bank conflicts in phase A's lookups
+#endif
+__host__ __device__ __forceinline__ int t2d_swz(int p) { return T2D_SWZ ? ((p >> 2) & 15) : 0; }
 #ifndef FG_TMEM_EARLY
 #define FG_TMEM_EARLY 1  // accumulator TMEM loads issued before the taps (B alone 48.6 -> 46.9 ms / 18 cells)
 #endif
@@ -348,7 +352,7 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
                             for (int a = 0; a < 4; ++a) {
                                 const int pu = (pu0 + a * dua + b * dub) & (FN - 1);
                                 const int pw = (pw0 + a * dwa + b * dwb) & (FN - 1);
-                                const double tv = t2[pu * FN + pw];
+                                const double tv = t2[pu * FN + (pw ^ t2d_swz(pu))];
                                 const double2 x = stg[(yl + 16 * b) * FN + zl + 16 * a];
                                 v[a + 4 * b] = make_double2(x.x * tv, x.y * tv);
                             }
@@ -571,7 +575,8 @@ __global__ void k_fg_t2d(int N, int nloc, const int *local, const int *row_off, 
             acc += cospi(2.0 * ph / N);
         }
     }
-    out[gid] = acc;
+    // stored with the row-dependent column swizzle of phase A's lookups (T2D_SWZ)
+    out[(int64_t)k * N * N + p * N + (q ^ t2d_swz(p))] = acc;
 }
 
 dvm_status_t build_fg_tables(dvm_plan_s *P)
