@@ -45,6 +45,9 @@ constexpr int FMS = 32;          // tap table size (2 M_e <= 32)
 #ifndef FG_BULK
 #define FG_BULK 1  // phase-A plane / T2D loads as one bulk copy each (mbarrier) instead of cp.async
 #endif
+#ifndef FG_BULKST
+#define FG_BULKST 1  // phase A writes each finished plane to the ring with bulk stores (TMA engine)
+#endif
 #ifndef T2D_SWZ
 #define T2D_SWZ 1  // XOR column swizzle of the T2D_e table: fewer bank conflicts in phase A's lookups
 #endif
@@ -380,6 +383,9 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
                     for (int n = 0; n < 16; ++n)
                         v[n] = x1w[(c_me >> 2) * 16 * FN + 16 * (c_me & 3) + (n ^ sw)];
                     idft16(v);  // z = kp1 + 4 kp2: v[kp2], kp1 = c_me & 3
+#if FG_BULKST
+                    if (warp == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // ex is read
+#endif
                     role_sync(bar);  // [2] staging and the exchange buffer are free
 #if FG_BULK
                     if (!lastp)
@@ -408,10 +414,42 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
                         for (int n = 0; n < 16; ++n) v[n] = src[n * FN];
                     }
                     idft16(v);  // y = kq1r + 4 kq2: v[kq2]
+#if FG_BULKST
+                    // back into the entries this thread read (row kq2 of quarter kq1r = ring row
+                    // y = kq1r + 4 kq2), then warp 0 bulk-stores the 64 rows (1 KB each)
+                    {
+                        double2 *own = ex + kq1r * F2Q + zr;
+#pragma unroll
+                        for (int k = 0; k < 16; ++k) own[k * FN] = v[k];
+                    }
+                    role_sync(bar);  // [4]
+                    if (warp == 0) {
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int idx = lane + 32 * h, q = idx >> 4, r = idx & 15;
+                            asm volatile(
+                                "cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(
+                                    Tb + (int64_t)g * FN2 + (q + 4 * r) * FN),
+                                "r"((uint32_t)__cvta_generic_to_shared(ex + q * F2Q + r * FN)),
+                                "r"((uint32_t)(sizeof(double2) * FN)), "l"(keep)
+                                : "memory");
+                        }
+                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    }
+#else
                     double2 *dst = Tb + (int64_t)g * FN2 + zr;
 #pragma unroll
                     for (int k = 0; k < 16; ++k) st2_hint(dst + (kq1r + 4 * k) * FN, v[k], keep);
+#endif
                 }
+#if FG_BULKST
+                if (warp == 0) {
+                    // the step's planes are in global memory before the release below
+                    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+                    asm volatile("fence.proxy.async.global;" ::: "memory");
+                }
+#endif
                 role_signal(cA + rank, stepi + 1, leader, bar);
             }
         }
