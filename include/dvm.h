@@ -225,7 +225,10 @@ DVM_API const char *dvm_profile_name(int k);
  * pair order (two launches, no FFT), 6 = 3D N = 32: two directions of one
  * cell per complex transform, T_a + i T_b = IFFT(f̂ (t̂_a + i t̂_b)), all
  * direction pairs in one batch plus the loss array f̂ λ̂ (auto for batches of
- * <= 2 cells at N = 32), 3 = the spectral reference
+ * <= 2 cells at N = 32), 7 = 2D tiles: one CTA per 16 x 32 node tile with a
+ * halo of Ñ in shared memory evaluates every pair unit's windows per node,
+ * Q = −fΛ + G (auto for 2D batches with >= 96 tiles when the tile fits shared
+ * memory, e.g. c3), 3 = the spectral reference
  * path (per direction one inverse transform gives
  * S_e + i T_e from the real filter spectra; a second cross-check, slow:
  * A inverse FFTs per cell; its tables need 16 A N^d bytes, <= 4 GB).  The FFT-loss paths evaluate
@@ -260,6 +263,7 @@ DVM_API dvm_status_t dvm_set_weights(dvm_plan_t plan, const double *a_box, const
 /* Tuning and timing switches of a plan (never read from the environment):
  *   "max_groups" cap on concurrent cell groups of the persistent 3D kernels
  *                (0 = every group that fits, the default)
+ *   "ring_slots" 3D N = 64 kernel: T_e ring slots per cell group, 2 (default) to 4
  *   "g3_cl"      frame-plane kernel CTAs per cell group at N = 32: 4, 8
  *                (default) or 16
  *   "verbose"    1 = print launch geometry on stderr

@@ -583,9 +583,10 @@ dvm_status_t dvm_set_path(dvm_plan_t P, int path)
         set_error("NULL argument");
         return DVM_E_NULL;
     }
-    if (path < 0 || path > 6) {
-        set_error("path must be 0 (auto), 1 (v1 orbit sweeps), 2 (gain3d / pair2d), 3 (spectral reference), 4 "
-                  "(3D FFT gain), 5 (2D small grids) or 6 (3D N = 32 spectral direction pairs)");
+    if (path < 0 || path > 7) {
+        set_error("path must be 0 (auto), 1 (v1 orbit sweeps), 2 (gain3d / pair2d line walks), 3 (spectral "
+                  "reference), 4 (3D FFT gain), 5 (2D small grids), 6 (3D N = 32 spectral direction pairs) or 7 "
+                  "(2D tiles)");
         return DVM_E_STATE;
     }
     P->path_mode = path;
@@ -606,6 +607,9 @@ dvm_status_t dvm_set_tuning(dvm_plan_t P, const char *key, int value)
     if (k == "max_groups") {
         if (value < 0) return bad();
         P->tune.max_groups = value;
+    } else if (k == "ring_slots") {
+        if (value != 0 && (value < 2 || value > 4)) return bad();
+        P->tune.ring_slots = value;
     } else if (k == "g3_cl") {
         if (value != 0 && value != 4 && value != 8 && value != 16) return bad();
         P->tune.g3_cl = value;

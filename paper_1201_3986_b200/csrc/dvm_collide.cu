@@ -412,7 +412,7 @@ dvm_status_t collide_batched(dvm_plan_s *P, const double *f, double *Q, int64_t 
     // N = 256 and at N = 128 with >= 100 directions of this plan's shard, the
     // v1 sweeps otherwise (fewer, latency-bound launches)
     if (P->wt.on) {  // caller weights a(k) b(l): the spectral path evaluates them
-        if (P->path_mode == 1 || P->path_mode == 2 || P->path_mode == 4 || P->path_mode == 6) {
+        if (P->path_mode == 1 || P->path_mode == 2 || P->path_mode == 4 || P->path_mode == 6 || P->path_mode == 7) {
             set_error("custom weights (dvm_set_weights) are evaluated by the spectral path: dvm_set_path 0 or 3");
             return DVM_E_STATE;
         }
@@ -441,7 +441,8 @@ dvm_status_t collide_batched(dvm_plan_s *P, const double *f, double *Q, int64_t 
     // auto: the 2D pair kernels from N = 256, and at N = 128 once there are >= 100 directions
     // (tools/path128.py: N = 128 with N̄ = 7 (A = 72) v1 96 us vs 117, N̄ = 10 (A = 128) 131 vs 120)
     const bool pair_auto = P->N >= 256 || (P->N >= 128 && (int)P->local.size() >= 100);
-    const bool use_new = P->path_mode == 2 || P->path_mode == 4 || (P->path_mode == 0 && (P->d == 3 || pair_auto));
+    const bool use_new = P->path_mode == 2 || P->path_mode == 4 || P->path_mode == 7 ||
+                         (P->path_mode == 0 && (P->d == 3 || pair_auto));
     if (use_new) {
         bool handled = false;
         dvm_status_t st = P->d == 3 ? collide_gain3d(P, f, stride, Q, stride, ncells, &handled)

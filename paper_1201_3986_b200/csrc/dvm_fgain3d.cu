@@ -703,7 +703,7 @@ dvm_status_t collide_fgain3d(dvm_plan_s *P, const double *f, int64_t f_stride, d
     if ((st = grow(&w.g3_f, &w.g3_f_elems, (size_t)(npairs * FNODES), P->stream))) return st;
     if ((st = grow(&w.fg_fhat, &w.fg_fhat_elems, (size_t)(npairs * FNODES), P->stream))) return st;
     if ((st = grow(&w.g3_q, &w.g3_q_elems, (size_t)(nchunks * npairs * FNODES), P->stream))) return st;
-    const int slots = 2;  // ring depth: phase A runs at most one step ahead of phase B
+    const int slots = P->tune.ring_slots ? P->tune.ring_slots : 2;  // ring depth: A runs up to slots-1 steps ahead
     if ((st = grow(&w.g3_t, &w.g3_t_elems, (size_t)ngroups * slots * FNODES, P->stream))) return st;
     if ((st = grow(&w.g3_ctr, &w.g3_ctr_elems, (size_t)ngroups * 2 * CL, P->stream))) return st;
     if ((st = interleave_pairs(P, f, f_stride, ncells, FNODES, w.g3_f))) return st;

@@ -149,6 +149,7 @@ namespace dvm {
 struct Tuning {
     int fg_dbg = 0;      // k_fg2 timing bits: 1 skip B work, 2 skip A work, 4 skip taps (results wrong)
     int max_groups = 0;  // cap on concurrent cell groups of the persistent 3D kernels (0: all that fit)
+    int ring_slots = 0;  // c5 kernel ring depth per group (0: 2)
     int g3_cl = 0;       // frame-plane kernel CTAs per group at N = 32 (0: 8)
     int verbose = 0;     // launch geometry on stderr
 };

@@ -254,7 +254,8 @@ class Plan:
 
     def set_path(self, path: int):
         """0 = auto, 1 = v1 orbit sweeps, 2 = FFT-loss kernels (gain3d / pair2d),
-        3 = spectral reference, 4 = 3D N = 64 FFT gain, 5 = 2D small-grid pairs."""
+        3 = spectral reference, 4 = 3D N = 64 FFT gain, 5 = 2D small-grid pairs,
+        6 = 3D N = 32 spectral direction pairs, 7 = 2D tiles."""
         _check(load().dvm_set_path(self._h, int(path)), "dvm_set_path")
 
     def set_tuning(self, key: str, value: int):

@@ -741,3 +741,28 @@ def test_fg32_path_matches_oracle(Nbar, Nt, cells, shard):
     for c in range(cells):
         Qo, _, _ = oracle.collide(f[c], 3, 32, Nbar, Nt, 8.0, dirs=dirs, diagnostics=False)
         _assert_parity(q6[c], Qo[0], f"fg32 N̄={Nbar} Ñ={Nt} cell {c}")
+
+
+# ---------------------------------------------------------------- 2D tile kernel (path 7, auto for N >= 128)
+@pytest.mark.parametrize("N,Nbar,Nt,cells,shard", [(256, 16, 57, 1, None), (128, 10, 28, 2, None), (16, 4, 4, 3, None),
+                                                   (64, 8, 14, 2, (1, 3)), (128, 5, 20, 1, (2, 4))])
+def test_tile2d_path_matches_oracle(N, Nbar, Nt, cells, shard):
+    """dvm_set_path(7): one CTA per 16 x 16 tile with a halo of Ñ in shared
+    memory, every pair unit's windows per node, Q = −fΛ + G:
+    against the oracle (sampled nodes, every node for small grids), the line-walk
+    pair kernels (path 2), several cells and direction shards."""
+    f = np.stack([dvm_inputs.two_bumps(2, N, 8.0, 0.8 + 0.3 * c, 0.01, 60 + c).reshape(-1) for c in range(cells)])
+    kw = {} if shard is None else {"shard_rank": shard[0], "shard_world": shard[1]}
+    p = _plan(2, N, Nbar, Ntilde=Nt, **kw)
+    p.set_path(7)
+    q7 = _gpu(p, f)
+    assert np.array_equal(q7, _gpu(p, f))
+    p.set_path(2)
+    q2 = _gpu(p, f)
+    np.testing.assert_allclose(q7, q2, rtol=0, atol=1e-13 * np.abs(q2).max())
+    pts = None if N ** 2 <= 4096 else np.arange(0, N ** 2, N ** 2 // 211)
+    dirs = p.directions()[0][p.directions()[3]] if shard else None
+    for c in range(cells):
+        Qo, _, _ = oracle.collide(f[c], 2, N, Nbar, Nt, 8.0, points=pts, dirs=dirs, diagnostics=False)
+        qc = q7[c] if pts is None else q7[c][pts]
+        _assert_parity(qc, Qo[0], f"tile2d N={N} cell {c}")

@@ -17,6 +17,9 @@ dbgs = [int(x) for x in sys.argv[2:]]
 reps = int(os.environ.get("REPS", "4"))
 f = torch.from_numpy(dvm_inputs.make("c5", cells=cells)).cuda()
 p = Plan(3, 64, 8)
+for kv in os.environ.get("TUNE", "").split():
+    k, v = kv.split("=")
+    p.set_tuning(k, int(v))
 
 
 def timed(p):
