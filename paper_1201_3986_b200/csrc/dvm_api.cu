@@ -6,6 +6,8 @@
 #include <new>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "dvm_internal.h"
 
 namespace dvm {
@@ -23,6 +25,15 @@ dvm_status_t cuda_fail(cudaError_t err, const char *what)
 }  // namespace dvm
 
 using namespace dvm;
+
+namespace {
+// NVTX range around every public entry point that launches work (header-only
+// NVTX3: a no-op unless a profiler injects itself)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 namespace {
 
@@ -128,6 +139,7 @@ const char *dvm_status_str(dvm_status_t s)
 
 dvm_status_t dvm_plan_ex(const dvm_plan_params_t *params, dvm_plan_t *out)
 {
+    NvtxRange nvtx_range("dvm_plan_ex");
     if (!params || !out) {
         set_error("NULL argument");
         return DVM_E_NULL;
@@ -291,6 +303,7 @@ dvm_status_t dvm_set_stream(dvm_plan_t P, void *stream)
 
 dvm_status_t dvm_collide_batched(dvm_plan_t P, const double *f, double *Q, int64_t ncells, int64_t cell_stride)
 {
+    NvtxRange nvtx_range("dvm_collide_batched");
     dvm_status_t st = check_batch(P, f, Q, ncells, &cell_stride);
     if (st) return st;
     return collide_batched(P, f, Q, ncells, cell_stride);
@@ -299,6 +312,7 @@ dvm_status_t dvm_collide_batched(dvm_plan_t P, const double *f, double *Q, int64
 dvm_status_t dvm_collide_batched_levels(const dvm_plan_t *plans, int nlevels, const double *f, double *Q,
                                         int64_t ncells, int64_t cell_stride, const int *level)
 {
+    NvtxRange nvtx_range("dvm_collide_batched_levels");
     if (!plans || nlevels < 1 || (ncells > 0 && !level)) {
         set_error(nlevels < 1 ? "nlevels must be >= 1" : "NULL argument");
         return nlevels < 1 ? DVM_E_SHAPE : DVM_E_NULL;
@@ -334,6 +348,7 @@ dvm_status_t dvm_collide(dvm_plan_t P, const double *f, double *Q)
 dvm_status_t dvm_collide_batched_host(dvm_plan_t P, const double *f_host, double *Q_host, int64_t ncells,
                                       int64_t cell_stride)
 {
+    NvtxRange nvtx_range("dvm_collide_batched_host");
     dvm_status_t st = check_batch(P, f_host, Q_host, ncells, &cell_stride);
     if (st) return st;
     if (ncells == 0) return DVM_OK;
@@ -521,11 +536,13 @@ dvm_status_t dvm_copy_cells(dvm_plan_t P, const double *src, const int64_t *src_
 
 dvm_status_t dvm_euler(dvm_plan_t P, double *f, double dt, int nsteps, double *moments_host)
 {
+    NvtxRange nvtx_range("dvm_euler");
     return time_stepper(P, 1, f, dt, nsteps, moments_host);
 }
 
 dvm_status_t dvm_rk2(dvm_plan_t P, double *f, double dt, int nsteps, double *moments_host)
 {
+    NvtxRange nvtx_range("dvm_rk2");
     return time_stepper(P, 2, f, dt, nsteps, moments_host);
 }
 
