@@ -347,7 +347,10 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
     e2e_value = global_cells * e2e_steps / (e2e_ms / 1e3)
-    same = bool(torch.equal(qh, Q.cpu()))
+    # the host variant evaluates large batches in 4 pipelined chunks: equal to the
+    # device-resident call up to fp64 summation order (direction chunking)
+    qd = Q.cpu()
+    e2e_rel = float((qh - qd).abs().max() / qd.abs().max()) if cells else 0.0
 
     clocks = clk.summary()
     if rank == 0:
@@ -362,7 +365,8 @@ def run_ours(args):
                            "effective_streaming_GBps_per_gpu": eff_step_gbs},
                 "roofline": roofline, "cpu_baseline": cpu,
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(fh.numel() * 8),
-                        "d2h_bytes_per_step": int(qh.numel() * 8), "matches_device_result": same},
+                        "d2h_bytes_per_step": int(qh.numel() * 8), "max_rel_diff_vs_device": e2e_rel,
+                        "pipelined": "4 chunks, copies on 2 streams" if cells >= 256 else "one shot"},
                 "gpu_launches": int(launches), "clocks": clocks,
                 "checks": {"mass_rel_max": mass_rel},
                 "kernel_profile_ms": {k: v[0] / psteps for k, v in prof.items() if v[1]}}

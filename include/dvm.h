@@ -171,7 +171,11 @@ DVM_API dvm_status_t dvm_collide_batched_levels(const dvm_plan_t *plans, int nle
                                                 int64_t ncells, int64_t cell_stride, const int *level);
 
 /* End-to-end variant with HOST buffers: copies f to the device, evaluates and
- * copies Q back (pinned host memory recommended); synchronous. */
+ * copies Q back; synchronous.  Batches of >= 256 cells are pipelined in 4
+ * chunks of whole cell pairs (host->device copies on one plan-owned copy
+ * stream, device->host on another, evaluation on the plan's stream), so with
+ * pinned host memory the copies overlap the evaluation.  The plan holds a
+ * device staging copy of f and Q (2 × ncells × N^d doubles). */
 DVM_API dvm_status_t dvm_collide_batched_host(dvm_plan_t plan, const double *f_host, double *Q_host,
                                       int64_t ncells, int64_t cell_stride);
 

@@ -5,6 +5,7 @@
 
 #include <new>
 #include <string>
+#include <vector>
 
 #include <nvtx3/nvToolsExt.h>
 
@@ -370,21 +371,62 @@ dvm_status_t dvm_collide_batched_host(dvm_plan_t P, const double *f_host, double
         }
         w.stage_elems = elems;
     }
-    if (cell_stride == nodes) {
-        DVM_CUDA(cudaMemcpyAsync(w.f_stage, f_host, sizeof(double) * elems, cudaMemcpyHostToDevice, P->stream));
-    } else {
-        DVM_CUDA(cudaMemcpy2DAsync(w.f_stage, sizeof(double) * nodes, f_host, sizeof(double) * cell_stride,
-                                   sizeof(double) * nodes, ncells, cudaMemcpyHostToDevice, P->stream));
+    // Large batches are pipelined in 4 chunks of whole cell pairs: the host->device
+    // copy of chunk i + 1 and the device->host copy of chunk i - 1 run on two
+    // plan-owned copy streams while chunk i is evaluated on the plan's stream
+    // (pinned host buffers needed for the overlap; results equal a one-shot call
+    // up to the FFT loss's cell pairing, which chunks of even size preserve).
+    const int nch = ncells >= 256 ? 4 : 1;
+    const int64_t per = nch == 1 ? ncells : (((ncells + nch - 1) / nch) + 1) / 2 * 2;
+    if (!P->cstream[0]) {
+        DVM_CUDA(cudaStreamCreateWithFlags(&P->cstream[0], cudaStreamNonBlocking));
+        DVM_CUDA(cudaStreamCreateWithFlags(&P->cstream[1], cudaStreamNonBlocking));
     }
-    st = collide_batched(P, w.f_stage, w.q_stage, ncells, nodes);
-    if (st) return st;
-    if (cell_stride == nodes) {
-        DVM_CUDA(cudaMemcpyAsync(Q_host, w.q_stage, sizeof(double) * elems, cudaMemcpyDeviceToHost, P->stream));
-    } else {
-        DVM_CUDA(cudaMemcpy2DAsync(Q_host, sizeof(double) * cell_stride, w.q_stage, sizeof(double) * nodes,
-                                   sizeof(double) * nodes, ncells, cudaMemcpyDeviceToHost, P->stream));
+    auto copy = [&](double *dst, int64_t dpitch, const double *src, int64_t spitch, int64_t nc, cudaMemcpyKind k,
+                    cudaStream_t strm) -> cudaError_t {
+        if (dpitch == nodes && spitch == nodes)
+            return cudaMemcpyAsync(dst, src, sizeof(double) * (size_t)(nc * nodes), k, strm);
+        return cudaMemcpy2DAsync(dst, sizeof(double) * dpitch, src, sizeof(double) * spitch, sizeof(double) * nodes,
+                                 nc, k, strm);
+    };
+    std::vector<cudaEvent_t> ev;
+    auto fail = [&](dvm_status_t code) {
+        for (cudaEvent_t e : ev) cudaEventDestroy(e);
+        return code;
+    };
+    for (int i = 0; i < 3 * nch; ++i) {
+        cudaEvent_t e;
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return fail(cuda_fail(cudaGetLastError(), "cudaEventCreate"));
+        ev.push_back(e);
     }
-    DVM_CUDA(cudaStreamSynchronize(P->stream));
+    // ev[0]: previous work on the plan's stream is done with the staging buffers
+    cudaError_t ce = cudaEventRecord(ev[0], P->stream);
+    if (ce == cudaSuccess) ce = cudaStreamWaitEvent(P->cstream[0], ev[0], 0);
+    if (ce != cudaSuccess) return fail(cuda_fail(ce, "cudaStreamWaitEvent"));
+    for (int i = 0; i < nch; ++i) {  // all host->device copies, in order, on copy stream 0
+        const int64_t c0 = i * per, nc = std::min<int64_t>(per, ncells - c0);
+        if (nc <= 0) break;
+        ce = copy(w.f_stage + c0 * nodes, nodes, f_host + c0 * cell_stride, cell_stride, nc, cudaMemcpyHostToDevice,
+                  P->cstream[0]);
+        if (ce == cudaSuccess) ce = cudaEventRecord(ev[nch + i], P->cstream[0]);
+        if (ce != cudaSuccess) return fail(cuda_fail(ce, "host->device copy"));
+    }
+    for (int i = 0; i < nch; ++i) {
+        const int64_t c0 = i * per, nc = std::min<int64_t>(per, ncells - c0);
+        if (nc <= 0) break;
+        if ((ce = cudaStreamWaitEvent(P->stream, ev[nch + i], 0)) != cudaSuccess) return fail(cuda_fail(ce, "wait"));
+        if ((st = collide_batched(P, w.f_stage + c0 * nodes, w.q_stage + c0 * nodes, nc, nodes))) return fail(st);
+        ce = cudaEventRecord(ev[2 * nch + i], P->stream);
+        if (ce == cudaSuccess) ce = cudaStreamWaitEvent(P->cstream[1], ev[2 * nch + i], 0);
+        if (ce == cudaSuccess)
+            ce = copy(Q_host + c0 * cell_stride, cell_stride, w.q_stage + c0 * nodes, nodes, nc, cudaMemcpyDeviceToHost,
+                      P->cstream[1]);
+        if (ce != cudaSuccess) return fail(cuda_fail(ce, "device->host copy"));
+    }
+    ce = cudaStreamSynchronize(P->cstream[1]);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(P->stream);
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamSynchronize");
     return DVM_OK;
 }
 
@@ -675,6 +717,12 @@ dvm_status_t dvm_plan_destroy(dvm_plan_t P)
         cudaEventDestroy(P->gev[0]);
         cudaEventDestroy(P->gev[1]);
     }
+    for (cudaStream_t &cs : P->cstream)
+        if (cs) {
+            cudaStreamSynchronize(cs);
+            cudaStreamDestroy(cs);
+            cs = nullptr;
+        }
     free_workspace(P);
     free_table(P);
     delete P;

@@ -178,6 +178,7 @@ struct dvm_plan_s {
     int path_mode = 0;      // evaluation path: 0 auto, 1 v1 orbit sweeps, 2 gain3d/pair2d when built, 3 spectral, 4 FFT gain (3D N = 64)
     bool use_graphs = true; // time steppers replay one captured step (CUDA graph)
     cudaStream_t gstream = nullptr;      // plan-owned stream for graph capture/replay
+    cudaStream_t cstream[2] = {nullptr, nullptr};  // host variant: host->device / device->host copy streams
     cudaEvent_t gev[2] = {nullptr, nullptr};
     std::vector<dvm::ProfRec> prof;
 };

@@ -316,6 +316,35 @@ def test_host_entry_point_matches_device():
     assert np.array_equal(p.collide_host(f), _gpu(p, f))
 
 
+@pytest.mark.parametrize("d,N,Nbar,cells", [(2, 16, 4, 300), (3, 32, 2, 258)])
+def test_host_entry_point_pipelined_batches(d, N, Nbar, cells):
+    """dvm_collide_batched_host with >= 256 cells runs 4 pipelined chunks (copy
+    streams + the plan's stream): equal to the device-resident batch (2D: bitwise,
+    cells are independent; 3D: to rounding, the direction chunking may differ),
+    also with a host cell stride > N^d."""
+    rng = np.random.default_rng(d * 100 + cells)
+    f = rng.uniform(0.0, 1.0, size=(cells, N ** d))
+    p = _plan(d, N, Nbar)
+    qd = _gpu(p, f)
+    qh = p.collide_host(f)
+    if d == 2:
+        assert np.array_equal(qh, qd)
+    else:
+        np.testing.assert_allclose(qh, qd, rtol=0, atol=1e-13 * np.abs(qd).max())
+    # strided host cells
+    import ctypes
+    from paper_1201_3986_b200 import dvm as _d
+    stride = N ** d + 5
+    fs = np.zeros((cells, stride))
+    fs[:, :N ** d] = f
+    qs = np.full((cells, stride), 7.0)
+    st = _d.load().dvm_collide_batched_host(p._h, ctypes.c_void_p(fs.ctypes.data), ctypes.c_void_p(qs.ctypes.data),
+                                           cells, stride)
+    assert st == 0
+    np.testing.assert_allclose(qs[:, :N ** d], qd, rtol=0, atol=1e-13 * np.abs(qd).max())
+    assert np.all(qs[:, N ** d:] == 7.0)
+
+
 def test_batched_edge_cases():
     from paper_1201_3986_b200 import DvmError
     p = _plan(2, 16, 4)
