@@ -48,6 +48,9 @@ constexpr int FMS = 32;          // tap table size (2 M_e <= 32)
 #ifndef FG_BULKST
 #define FG_BULKST 1  // phase A writes each finished plane to the ring with bulk stores (TMA engine)
 #endif
+#ifndef FG_BDEC
+#define FG_BDEC 1  // phase B's x-exchange ordered by mbarriers, stage 1 of batch b+1 before the taps of b
+#endif
 #ifndef T2D_SWZ
 #define T2D_SWZ 1  // XOR column swizzle of the T2D_e table: fewer bank conflicts in phase A's lookups
 #endif
@@ -200,6 +203,10 @@ __device__ __forceinline__ void mbar_init(uint64_t *m, int count)
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(m)), "r"(count)
                  : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t *m)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((uint32_t)__cvta_generic_to_shared(m)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t *m, uint32_t phase)
 {
     const uint32_t a = (uint32_t)__cvta_generic_to_shared(m);
@@ -241,6 +248,7 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
     __shared__ uint32_t soff[2][FMS];
     __shared__ uint32_t s_tmem;
     __shared__ __align__(8) uint64_t s_mbar;  // FG_BULK: completion of the phase-A bulk loads
+    __shared__ __align__(8) uint64_t s_xbar[2], s_rbar[2];  // FG_BDEC: exchange buffer written / read
 
     const bool roleA = threadIdx.x < kRoleT;
     const int t = threadIdx.x & (kRoleT - 1);
@@ -268,6 +276,10 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
     }
     if (threadIdx.x == 0) {
         mbar_init(&s_mbar, 1);
+        for (int k = 0; k < 2; ++k) {
+            mbar_init(&s_xbar[k], kRoleT);
+            mbar_init(&s_rbar[k], kRoleT);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -484,6 +496,50 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
 #pragma unroll
                     for (int n2 = 0; n2 < 8; ++n2) pre[n2] = ld2_cg_hint(Tb + ((int64_t)(warp + 8 * n2) * FN + y) * FN + z, drop);
                 };
+#if FG_BDEC
+                // stage 1 of a batch (DFT-8 over n2, twiddle) from the prefetched ring values
+                // into exchange buffer b & 1, then every B thread arrives on s_xbar[b & 1];
+                // stage 2 waits on that barrier only, and arrives on s_rbar[b & 1] once read.
+                // Each buffer completes 4 phases per step: parity (b >> 1) & 1.
+                auto stage1 = [&](int b) {
+                    const int y = FRY * rank + (b >> 1);
+                    double2 u[8];
+#pragma unroll
+                    for (int n2 = 0; n2 < 8; ++n2) u[n2] = pre[n2];
+                    idft8(u);
+#pragma unroll
+                    for (int k2 = 1; k2 < 8; ++k2) u[k2] = cmul(u[k2], tw[(warp * k2) & (FN - 1)]);
+                    double2 *Rw = rb + (b & 1) * FN * 32;
+#pragma unroll
+                    for (int k2 = 0; k2 < 8; ++k2) Rw[(warp + 8 * k2) * 32 + lane] = u[k2];
+                    __syncwarp();
+                    const double2 *line = Tb + ((int64_t)(warp + 8 * (lane >> 2)) * FN + y) * FN + 32 * (b & 1) + 8 * (lane & 3);
+                    asm volatile("discard.global.L2 [%0], 128;" ::"l"(line) : "memory");
+                    mbar_arrive(&s_xbar[b & 1]);
+                };
+                if (!(A.dbg & 1)) {
+                    fetch(0);
+                    stage1(0);
+                    fetch(1);
+                }
+#pragma unroll 1
+                for (int b = 0; b < ((A.dbg & 1) ? 0 : (2 * FRY)); ++b) {
+                    const int y = FRY * rank + (b >> 1), z = 32 * (b & 1) + lane;
+                    double2 v[8];
+                    const double2 *R = rb + (b & 1) * FN * 32;
+                    mbar_wait(&s_xbar[b & 1], (uint32_t)((b >> 1) & 1));
+                    const int k2 = warp;
+#pragma unroll
+                    for (int n1 = 0; n1 < 8; ++n1) v[n1] = R[(n1 + 8 * k2) * 32 + lane];
+                    mbar_arrive(&s_rbar[b & 1]);
+                    idft8(v);  // v[k1] = N^3 T_e(x = k2 + 8 k1, y, z)
+                    if (b + 1 < (2 * FRY)) {
+                        // buffer (b + 1) & 1 was batch b - 1's: wait until every thread has read it
+                        if (b >= 1) mbar_wait(&s_rbar[(b + 1) & 1], (uint32_t)(((b - 1) >> 1) & 1));
+                        stage1(b + 1);
+                        if (b + 2 < (2 * FRY)) fetch(b + 2);
+                    }
+#else
                 if (!(A.dbg & 1)) fetch(0);
 #pragma unroll 1
                 for (int b = 0; b < ((A.dbg & 1) ? 0 : (2 * FRY)); ++b) {
@@ -513,6 +569,7 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
 #pragma unroll
                     for (int n1 = 0; n1 < 8; ++n1) v[n1] = R[(n1 + 8 * k2) * 32 + lane];
                     idft8(v);  // v[k1] = N^3 T_e(x = k2 + 8 k1, y, z)
+#endif
 #pragma unroll
                     for (int hh = 0; hh < 2; ++hh) {
                         uint32_t n[4];
