@@ -234,26 +234,36 @@ __global__ void k_moments_partial(const double *__restrict__ f, Geo g, double h,
         for (int k = 0; k < K; ++k) partial[blockIdx.x * K + k] = sm[k][0];
 }
 
-__global__ void k_moments_final(const double *partial, int nblocks, double scale, double *out)
+// The kMomBlocks block partials of each moment added by a fixed-order tree in
+// shared memory (one thread per partial; kMomBlocks = 128 threads).
+__device__ __forceinline__ void moments_tree(const double *partial, int nblocks, double scale, double *out)
 {
     constexpr int K = kMaxD + 2;
-    if (threadIdx.x < K) {
-        double s = 0.0;
-        for (int b = 0; b < nblocks; ++b) s += partial[b * K + threadIdx.x];
-        out[threadIdx.x] = s * scale;
+    __shared__ double sm[K][kMomBlocks];
+    const int t = threadIdx.x;
+    for (int k = 0; k < K; ++k) sm[k][t] = t < nblocks ? partial[t * K + k] : 0.0;
+    __syncthreads();
+    for (int s = kMomBlocks / 2; s > 0; s >>= 1) {
+        if (t < s)
+            for (int k = 0; k < K; ++k) sm[k][t] += sm[k][t + s];
+        __syncthreads();
     }
+    if (t < K) out[t] = sm[t][0] * scale;
+}
+
+__global__ void __launch_bounds__(kMomBlocks) k_moments_final(const double *partial, int nblocks, double scale,
+                                                              double *out)
+{
+    moments_tree(partial, nblocks, scale, out);
 }
 
 // moments row selected by a device counter (graph-replayable): out[ctr] = ..., ctr++
-__global__ void k_moments_final_ctr(const double *partial, int nblocks, double scale, double *base, int *ctr)
+__global__ void __launch_bounds__(kMomBlocks) k_moments_final_ctr(const double *partial, int nblocks, double scale,
+                                                                  double *base, int *ctr)
 {
     constexpr int K = kMaxD + 2;
     const int row = *ctr;
-    if (threadIdx.x < K) {
-        double s = 0.0;
-        for (int b = 0; b < nblocks; ++b) s += partial[b * K + threadIdx.x];
-        base[(size_t)row * K + threadIdx.x] = s * scale;
-    }
+    moments_tree(partial, nblocks, scale, base + (size_t)row * K);
     __syncthreads();
     if (threadIdx.x == 0) *ctr = row + 1;
 }
@@ -513,7 +523,7 @@ dvm_status_t moments(dvm_plan_s *P, const double *f, double *dev_out_row)
     }
     {
         LaunchScope ls(P, KC_MOMENTS);
-        k_moments_final<<<1, 32, 0, P->stream>>>(P->ws.mom_partial, kMomBlocks, scale, dev_out_row);
+        k_moments_final<<<1, kMomBlocks, 0, P->stream>>>(P->ws.mom_partial, kMomBlocks, scale, dev_out_row);
     }
     DVM_CUDA(cudaGetLastError());
     return DVM_OK;
@@ -531,7 +541,8 @@ dvm_status_t moments_ctr(dvm_plan_s *P, const double *f, double *dev_base, int *
     }
     {
         LaunchScope ls(P, KC_MOMENTS);
-        k_moments_final_ctr<<<1, 32, 0, P->stream>>>(P->ws.mom_partial, kMomBlocks, scale, dev_base, dev_ctr);
+        k_moments_final_ctr<<<1, kMomBlocks, 0, P->stream>>>(P->ws.mom_partial, kMomBlocks, scale, dev_base,
+                                                             dev_ctr);
     }
     DVM_CUDA(cudaGetLastError());
     return DVM_OK;
