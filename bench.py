@@ -109,13 +109,18 @@ def _dist():
     return world, rank, local
 
 
-def _oracle_sample(name: str, seconds: float, seed: int):
+_NPAIRS = {}
+
+
+def _oracle_sample(name: str, seconds: float, seed: int, k_fixed: int | None = None):
     """Time the oracle (oracle/dvm_oracle.c as it stands) on a bounded sample of
     workload `name`: whole-grid evaluations when the grid is small, otherwise a
     seeded set of nodes of one cell sized for ~`seconds` of host work.  The
     oracle hands out blocks of 16 nodes per thread (OpenMP dynamic), so the
     sample is a multiple of 16 x threads nodes and every thread is busy.
-    Returns (evals/s, busy threads, sample description, seconds)."""
+    k_fixed: a sample size (in blocks of 16 x threads nodes) from an earlier
+    call, skipping the calibration.
+    Returns (evals/s, busy threads, sample description, seconds, k)."""
     import dvm_inputs
     from oracle import oracle
     cfg = dvm_inputs.CONFIGS[name]
@@ -124,7 +129,9 @@ def _oracle_sample(name: str, seconds: float, seed: int):
     f = dvm_inputs.make(name, cells=1)[0]
     threads = os.cpu_count() or 1
     block = 16 * threads
-    npairs = oracle.pairs(cfg.d, Nt, cfg.Nbar, 1.0)[2].size
+    if name not in _NPAIRS:
+        _NPAIRS[name] = oracle.pairs(cfg.d, Nt, cfg.Nbar, 1.0)[2].size
+    npairs = _NPAIRS[name]
     if nodes <= 4 * block:
         t0 = time.perf_counter()
         oracle.collide(f, cfg.d, cfg.N, cfg.Nbar, Nt, cfg.L, diagnostics=False)
@@ -136,24 +143,32 @@ def _oracle_sample(name: str, seconds: float, seed: int):
         dt = time.perf_counter() - t0
         busy = min(threads, -(-nodes // 16))
         return reps / dt, busy, (f"{reps} whole-grid evaluations of {name} ({nodes} nodes, {npairs} pairs/node), "
-                                 f"{dt:.1f} s"), dt
+                                 f"{dt:.1f} s"), dt, None
     rng = np.random.default_rng(seed)
-    pts = np.sort(rng.choice(nodes, size=block, replace=False)).astype(np.int64)
-    t0 = time.perf_counter()
-    oracle.collide(f, cfg.d, cfg.N, cfg.Nbar, Nt, cfg.L, points=pts, diagnostics=False)
-    dt = time.perf_counter() - t0
-    k = int(max(1, min(nodes // block, seconds / max(dt, 1e-3))))
+    if k_fixed is None:
+        # per-call fixed cost (the oracle builds its pair list on every call) and the
+        # per-block cost, so the sample is sized on the node work
+        t0 = time.perf_counter()
+        oracle.collide(f, cfg.d, cfg.N, cfg.Nbar, Nt, cfg.L, points=np.zeros(1, np.int64), diagnostics=False)
+        t_fix = time.perf_counter() - t0
+        pts = np.sort(rng.choice(nodes, size=block, replace=False)).astype(np.int64)
+        t0 = time.perf_counter()
+        oracle.collide(f, cfg.d, cfg.N, cfg.Nbar, Nt, cfg.L, points=pts, diagnostics=False)
+        t_blk = max(time.perf_counter() - t0 - t_fix, 1e-3)
+        k = int(max(4, min(nodes // block, seconds / t_blk)))  # >= 4 blocks per thread: the pair list is amortised
+    else:
+        k = k_fixed
     pts = np.sort(rng.choice(nodes, size=k * block, replace=False)).astype(np.int64)
     t0 = time.perf_counter()
     oracle.collide(f, cfg.d, cfg.N, cfg.Nbar, Nt, cfg.L, points=pts, diagnostics=False)
     dt = time.perf_counter() - t0
     return ((pts.size / dt) / nodes, threads,
             f"{pts.size} seeded nodes of one {name} cell (of {nodes}), direct pair sum ({npairs} pairs/node), "
-            f"{dt:.1f} s; evals/s = nodes/s / {nodes}", dt)
+            f"{dt:.1f} s; evals/s = nodes/s / {nodes}", dt, k)
 
 
 def cpu_baseline(name: str = "c5", seconds: float = 15.0):
-    value, busy, sample, _ = _oracle_sample(name, seconds, 0)
+    value, busy, sample, _, _ = _oracle_sample(name, seconds, 0)
     return {"value": value, "unit": UNIT, "cores": busy, "kind": "oracle", "sample": sample}
 
 
@@ -162,13 +177,16 @@ def run_reference(args):
     if rank != 0:
         return 0
     name = args.workload
-    per_step_s = float(os.environ.get("REF_SECONDS_PER_STEP", "6"))
-    for _ in range(args.warmup):
-        _oracle_sample(name, 0.5, 99)
+    per_step_s = float(os.environ.get("REF_SECONDS_PER_STEP", "3"))
+    # calibrate the per-step sample once (warm-up), then time every step on it
+    kfix = None
+    for w in range(max(1, args.warmup)):
+        _, _, _, _, kk = _oracle_sample(name, per_step_s if w == 0 else 0.2, 99, kfix)
+        kfix = kk if kfix is None else kfix
     vals, secs = [], 0.0
     busy, sample = 0, ""
     for k in range(args.steps):
-        v, busy, sample, dt = _oracle_sample(name, per_step_s, 1 + k)
+        v, busy, sample, dt, _ = _oracle_sample(name, per_step_s, 1 + k, kfix)
         vals.append(v)
         secs += dt
     value = float(np.mean(vals))
