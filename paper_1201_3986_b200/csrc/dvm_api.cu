@@ -459,6 +459,16 @@ static dvm_status_t one_step(dvm_plan_s *P, int scheme, double *f, double dt, bo
     const int64_t nodes = nodes_of(P);
     Workspace &w = P->ws;
     dvm_status_t st;
+    // small 2D grids, Euler: unit sum, f += dt Q and the moments partials in one launch
+    if (scheme == 1 && !P->wt.on && (P->path_mode == 0 || P->path_mode == 5) && w.mom_partial) {
+        bool handled = false;
+        int nb = 0;
+        if ((st = euler_small2d(P, f, w.qtmp, dt, w.mom_partial, &nb, &handled))) return st;
+        if (handled) {
+            if (mom && (st = moments_final_ctr(P, nb, w.mom_dev, w.mom_ctr))) return st;
+            return DVM_OK;
+        }
+    }
     if ((st = collide_batched(P, f, w.qtmp, 1, nodes))) return st;
     if (scheme == 1) {
         if ((st = axpy(P, f, w.qtmp, dt))) return st;
@@ -499,6 +509,7 @@ static dvm_status_t time_stepper(dvm_plan_s *P, int scheme, double *f, double dt
     if (!w.qtmp) DVM_CUDA(cudaMalloc(&w.qtmp, sizeof(double) * nodes));
     if (scheme == 2 && !w.f1tmp) DVM_CUDA(cudaMalloc(&w.f1tmp, sizeof(double) * nodes));
     if (!w.mom_ctr) DVM_CUDA(cudaMalloc(&w.mom_ctr, sizeof(int)));
+    if (!w.mom_partial) DVM_CUDA(cudaMalloc(&w.mom_partial, sizeof(double) * 128 * (kMaxD + 2)));
     DVM_CUDA(cudaMemsetAsync(w.mom_ctr, 0, sizeof(int), P->stream));
     dvm_status_t st;
     if (mom && (st = moments_ctr(P, f, w.mom_dev, w.mom_ctr))) return st;

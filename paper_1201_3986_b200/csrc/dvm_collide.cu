@@ -529,6 +529,19 @@ dvm_status_t moments(dvm_plan_s *P, const double *f, double *dev_out_row)
     return DVM_OK;
 }
 
+// the final fixed-order tree over `nblocks` (<= kMomBlocks) partials already in ws.mom_partial
+dvm_status_t moments_final_ctr(dvm_plan_s *P, int nblocks, double *dev_base, int *dev_ctr)
+{
+    double scale = 1.0;
+    for (int j = 0; j < P->d; ++j) scale *= P->h;
+    {
+        LaunchScope ls(P, KC_MOMENTS);
+        k_moments_final_ctr<<<1, kMomBlocks, 0, P->stream>>>(P->ws.mom_partial, nblocks, scale, dev_base, dev_ctr);
+    }
+    DVM_CUDA(cudaGetLastError());
+    return DVM_OK;
+}
+
 dvm_status_t moments_ctr(dvm_plan_s *P, const double *f, double *dev_base, int *dev_ctr)
 {
     const Geo g = geo_of(P);

@@ -274,6 +274,11 @@ dvm_status_t build_gain3d(dvm_plan_s *P);
 dvm_status_t build_pair2d(dvm_plan_s *P);
 dvm_status_t collide_small2d(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q, int64_t q_stride,
                              int64_t ncells, bool *handled);
+// one explicit Euler step of one small 2D cell with the unit sum, f += dt Q and
+// the moments partials fused (handled = false: use the general path)
+dvm_status_t euler_small2d(dvm_plan_s *P, double *f, double *Q, double dt, double *mpart, int *nblocks,
+                           bool *handled);
+dvm_status_t moments_final_ctr(dvm_plan_s *P, int nblocks, double *dev_base, int *dev_ctr);
 dvm_status_t collide_pair2d(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q, int64_t q_stride,
                             int64_t ncells, bool *handled);
 void free_gain3d(dvm_plan_s *P);

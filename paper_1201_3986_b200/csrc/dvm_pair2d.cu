@@ -267,6 +267,56 @@ __global__ void __launch_bounds__(256) k_small2d_sum(const double *__restrict__ 
     }
 }
 
+// The same sum for one cell fused with an explicit Euler step and the moments
+// partials of the new f (time stepping of small grids, config c2): Q is written,
+// f <- f + dt Q exactly as k_axpy does, and every block (32 nodes) writes its
+// mass / momentum / energy partial sums (reading R16; a fixed xor-shuffle tree)
+// for the final fixed-order tree of dvm_collide.cu.  One launch instead of three.
+__global__ void __launch_bounds__(256) k_small2d_sum_euler(const double *__restrict__ part, int nunits, int nodes,
+                                                           double *__restrict__ Q, double *__restrict__ f,
+                                                           double dt, int p, int N, double h,
+                                                           double *__restrict__ mpart)
+{
+    __shared__ double gs[8][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int per = (nunits + 7) / 8, u0 = min(nunits, w * per), u1 = min(nunits, u0 + per);
+    const int i = blockIdx.x * 32 + lane;
+    double acc = 0.0;
+    if (i < nodes) {
+        const double *pc = part + i;
+#pragma unroll 4
+        for (int uu = u0; uu < u1; ++uu) acc += pc[(int64_t)uu * nodes];
+    }
+    gs[w][lane] = acc;
+    __syncthreads();
+    if (w == 0) {
+        double m[4] = {0.0, 0.0, 0.0, 0.0};
+        if (i < nodes) {
+            double q = 0.0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) q += gs[k][lane];
+            Q[i] = q;
+            const double fn = f[i] + dt * q;
+            f[i] = fn;
+            const double v0 = ((i >> p) - N / 2) * h, v1 = ((i & (N - 1)) - N / 2) * h;
+            m[0] = fn;
+            m[1] = v0 * fn;
+            m[2] = v1 * fn;
+            m[3] = (v0 * v0 + v1 * v1) * fn;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) m[k] += __shfl_xor_sync(0xffffffffu, m[k], o);
+        if (lane == 0) {
+            double *mp = mpart + (int64_t)blockIdx.x * 5;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) mp[k] = m[k];
+            mp[4] = 0.0;
+        }
+    }
+}
+
 // ---------------------------------------------------------------- 2D tile kernel (N >= 128)
 // One CTA per 16 x 32 node tile and cell (a warp per tile row): the tile plus a halo of Ñ (every
 // window offset m e has |m e|_inf <= M_e |e|_inf <= Ñ) is loaded into shared
@@ -341,6 +391,31 @@ size_t tile2d_smem(int Ntilde, int nunits)
     return sizeof(double) * (size_t)((PR * P + 1) & ~1) + sizeof(Unit2D) * (size_t)nunits;
 }
 
+// the per-unit partials of one cell (k_small2d only), into P->ws.p2_part
+dvm_status_t collide_small2d_parts(dvm_plan_s *P, const double *f, bool *handled);
+
+dvm_status_t euler_small2d(dvm_plan_s *P, double *f, double *Q, double dt, double *mpart, int *nblocks,
+                           bool *handled)
+{
+    *handled = false;
+    if (P->d != 2 || P->N > 64 || !P->g.ready || P->g.nunits == 0 || !mpart) return DVM_OK;
+    const int N = P->N, nodes = N * N, nunits = P->g.nunits;
+    if ((nodes + 31) / 32 > 128) return DVM_OK;  // the moments tree holds 128 partials
+    bool h1 = false;
+    // the partials of one cell (k_small2d), then the fused sum + Euler + moments partials
+    dvm_status_t st = collide_small2d_parts(P, f, &h1);
+    if (st || !h1) return st;
+    {
+        LaunchScope ls(P, KC_REDUCE);
+        k_small2d_sum_euler<<<(nodes + 31) / 32, 256, 0, P->stream>>>(P->ws.p2_part, nunits, nodes, Q, f, dt, P->p,
+                                                                     N, P->h, mpart);
+        DVM_CUDA(cudaGetLastError());
+    }
+    *nblocks = (nodes + 31) / 32;
+    *handled = true;
+    return DVM_OK;
+}
+
 // small 2D grids (N <= 64): gain and loss per pair unit in shared memory, two launches
 dvm_status_t collide_small2d(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q, int64_t q_stride,
                              int64_t ncells, bool *handled)
@@ -378,6 +453,13 @@ dvm_status_t collide_small2d(dvm_plan_s *P, const double *f, int64_t f_stride, d
                                           (int)(sizeof(double) * 2 * 64 * 64)));
             done[dev] = 1;
         }
+    }
+    if (!Q) {  // collide_small2d_parts: the partials of one cell only
+        const int nslice = (int)std::max<int64_t>(1, std::min<int64_t>(8, sms / (int64_t)nunits));
+        LaunchScope ls(P, KC_SMALL2D);
+        k_small2d<<<dim3(nunits * nslice, 1), kST, smem, P->stream>>>(f, f_stride, units, nunits, nslice, p, w.p2_part);
+        DVM_CUDA(cudaGetLastError());
+        return DVM_OK;
     }
     for (int64_t c0 = 0; c0 < ncells; c0 += chunk) {
         const int nc = (int)std::min<int64_t>(chunk, ncells - c0);
@@ -462,6 +544,11 @@ dvm_status_t build_pair2d(dvm_plan_s *P)
 }
 
 size_t pair2d_unit_bytes() { return sizeof(Unit2D); }
+
+dvm_status_t collide_small2d_parts(dvm_plan_s *P, const double *f, bool *handled)
+{
+    return collide_small2d(P, f, P->N * P->N, nullptr, 0, 1, handled);
+}
 
 dvm_status_t collide_pair2d(dvm_plan_s *P, const double *f, int64_t f_stride, double *Q, int64_t q_stride,
                             int64_t ncells, bool *handled)
