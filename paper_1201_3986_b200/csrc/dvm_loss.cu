@@ -7,8 +7,9 @@
 //
 //   plan time   k_lambda (one thread per node, directions in order) and
 //               λ̂ = FFT(λ) with the passes below (k_take_real)
-//   per collide loss_init: d forward passes (the first reads f, the last
-//               multiplies by λ̂), d inverse passes (the last writes −f Λ)
+//   per collide loss_init: 2d − 1 passes: d − 1 forward, one along axis 0 that
+//               runs forward, × λ̂ and inverse in shared memory, d − 1
+//               inverse (the last writes −f Λ)
 // k_fft_pass is a radix-2 fp64 pass along one axis over tiles of lines in
 // shared memory, twiddles exp(−2πik/N) from sincospi.
 #include <math.h>
@@ -35,6 +36,7 @@ struct FftArgs {
     const double2 *zin;
     double2 *zout;
     const double *mult;  // optional real multiplier per node (λ̂)
+    int roundtrip;       // forward stages, × mult, inverse stages in one pass (the middle axis pair)
     // epilogue (last inverse pass): Q[c] = -f[c] * Λ[c]
     double *q;
     int64_t q_stride;
@@ -108,18 +110,45 @@ __global__ void __launch_bounds__(kFT) k_fft_pass(FftArgs A)
         buf[i * N + tr] = v;
     }
     __syncthreads();
-    for (int half = 1; half < N; half <<= 1) {
-        for (int b = threadIdx.x; b < B * N / 2; b += kFT) {
-            const int i = b / (N / 2), k = b % (N / 2);
-            const int pos = k & (half - 1), grp = k / half;
-            const int i0 = grp * 2 * half + pos, i1 = i0 + half;
-            double2 w = A.tw[pos * (N / (2 * half))];
-            if (A.inverse) w.y = -w.y;
-            const double2 u = buf[i * N + i0], v = cmul(buf[i * N + i1], w);
-            buf[i * N + i0] = make_double2(u.x + v.x, u.y + v.y);
-            buf[i * N + i1] = make_double2(u.x - v.x, u.y - v.y);
+    auto stages = [&](bool inverse) {
+        for (int half = 1; half < N; half <<= 1) {
+            for (int b = threadIdx.x; b < B * N / 2; b += kFT) {
+                const int i = b / (N / 2), k = b % (N / 2);
+                const int pos = k & (half - 1), grp = k / half;
+                const int i0 = grp * 2 * half + pos, i1 = i0 + half;
+                double2 w = A.tw[pos * (N / (2 * half))];
+                if (inverse) w.y = -w.y;
+                const double2 u = buf[i * N + i0], v = cmul(buf[i * N + i1], w);
+                buf[i * N + i0] = make_double2(u.x + v.x, u.y + v.y);
+                buf[i * N + i1] = make_double2(u.x - v.x, u.y - v.y);
+            }
+            __syncthreads();
+        }
+    };
+    stages(A.inverse != 0);
+    if (A.roundtrip) {
+        // the same arithmetic as a forward pass storing × λ̂ and an inverse pass
+        // loading bit-reversed: multiply, permute in shared memory, inverse stages
+        for (int idx = threadIdx.x; idx < B * N; idx += kFT) {
+            int i, t;
+            if (last_axis) { i = idx / N; t = idx % N; }
+            else { i = idx % B; t = idx / B; }
+            const double m = A.mult[addr(i, t)];
+            buf[i * N + t].x *= m;
+            buf[i * N + t].y *= m;
         }
         __syncthreads();
+        for (int idx = threadIdx.x; idx < B * N; idx += kFT) {
+            const int i = idx / N, t = idx % N;
+            const int tr = (int)(__brev((unsigned)t) >> (32 - LOGN));
+            if (t < tr) {
+                const double2 x = buf[i * N + t];
+                buf[i * N + t] = buf[i * N + tr];
+                buf[i * N + tr] = x;
+            }
+        }
+        __syncthreads();
+        stages(true);
     }
     for (int idx = threadIdx.x; idx < B * N; idx += kFT) {
         int i, t;
@@ -127,7 +156,7 @@ __global__ void __launch_bounds__(kFT) k_fft_pass(FftArgs A)
         else { i = idx % B; t = idx / B; }
         const int64_t a = addr(i, t);
         double2 v = buf[i * N + t];
-        if (A.mult) {
+        if (A.mult && !A.roundtrip) {
             const double m = A.mult[a];
             v.x *= m;
             v.y *= m;
@@ -630,6 +659,7 @@ dvm_status_t loss_init(dvm_plan_s *P, const double *f, int64_t f_stride, double 
     for (int64_t p0 = 0; p0 < npairs_all; p0 += batch) {
         const int64_t np = std::min(batch, npairs_all - p0);
         for (int k = 0; k < 2 * d; ++k) {
+            if (k == d) continue;  // the first inverse pass ran inside pass d - 1 (roundtrip)
             FftArgs a = {};
             a.d = d;
             a.npairs = np;
@@ -645,7 +675,10 @@ dvm_status_t loss_init(dvm_plan_s *P, const double *f, int64_t f_stride, double 
                 a.r0 = f;
                 a.r_stride = f_stride;
             }
-            if (k == d - 1) a.mult = lamhat;
+            if (k == d - 1) {
+                a.mult = lamhat;
+                a.roundtrip = 1;
+            }
             if (k == 2 * d - 1) {
                 a.qI = QI;
                 a.q = Q;
