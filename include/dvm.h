@@ -268,6 +268,8 @@ DVM_API dvm_status_t dvm_set_weights(dvm_plan_t plan, const double *a_box, const
  *   "max_groups" cap on concurrent cell groups of the persistent 3D kernels
  *                (0 = every group that fits, the default)
  *   "ring_slots" 3D N = 64 kernel: T_e ring slots per cell group, 2 (default) to 4
+ *   "fg_chunks"  3D N = 64 kernel: direction chunks per cell pair, 1 to 64
+ *                (0 = automatic, the default)
  *   "g3_cl"      frame-plane kernel CTAs per cell group at N = 32: 4, 8
  *                (default) or 16
  *   "verbose"    1 = print launch geometry on stderr

@@ -680,6 +680,9 @@ dvm_status_t dvm_set_tuning(dvm_plan_t P, const char *key, int value)
     } else if (k == "ring_slots") {
         if (value != 0 && (value < 2 || value > 4)) return bad();
         P->tune.ring_slots = value;
+    } else if (k == "fg_chunks") {
+        if (value < 0 || value > 64) return bad();
+        P->tune.fg_chunks = value;
     } else if (k == "g3_cl") {
         if (value != 0 && value != 4 && value != 8 && value != 16) return bad();
         P->tune.g3_cl = value;

@@ -469,6 +469,9 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
     } else {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegB2));
         const uint32_t tm_base = s_tmem + ((uint32_t)(32 * (warp & 3)) << 16) + 256u * (uint32_t)(warp >> 2);
+        // batch b -> (row, z half)
+        auto b_row = [](int b) { return b >> 1; };
+        auto b_zh = [](int b) { return b & 1; };
         for (int64_t item = grp; item < items; item += ngroups) {
             const int64_t pair = item / A.nchunks;
             const int chunk = (int)(item % A.nchunks);
@@ -492,7 +495,7 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
                 // ring columns straight into registers, one batch ahead (coalesced 512 B per warp row)
                 double2 pre[8];
                 auto fetch = [&](int b) {
-                    const int y = FRY * rank + (b >> 1), z = 32 * (b & 1) + lane;
+                    const int y = FRY * rank + b_row(b), z = 32 * b_zh(b) + lane;
 #pragma unroll
                     for (int n2 = 0; n2 < 8; ++n2) pre[n2] = ld2_cg_hint(Tb + ((int64_t)(warp + 8 * n2) * FN + y) * FN + z, drop);
                 };
@@ -502,7 +505,7 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
                 // stage 2 waits on that barrier only, and arrives on s_rbar[b & 1] once read.
                 // Each buffer completes 4 phases per step: parity (b >> 1) & 1.
                 auto stage1 = [&](int b) {
-                    const int y = FRY * rank + (b >> 1);
+                    const int y = FRY * rank + b_row(b);
                     double2 u[8];
 #pragma unroll
                     for (int n2 = 0; n2 < 8; ++n2) u[n2] = pre[n2];
@@ -513,7 +516,7 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
 #pragma unroll
                     for (int k2 = 0; k2 < 8; ++k2) Rw[(warp + 8 * k2) * 32 + lane] = u[k2];
                     __syncwarp();
-                    const double2 *line = Tb + ((int64_t)(warp + 8 * (lane >> 2)) * FN + y) * FN + 32 * (b & 1) + 8 * (lane & 3);
+                    const double2 *line = Tb + ((int64_t)(warp + 8 * (lane >> 2)) * FN + y) * FN + 32 * b_zh(b) + 8 * (lane & 3);
                     asm volatile("discard.global.L2 [%0], 128;" ::"l"(line) : "memory");
                     mbar_arrive(&s_xbar[b & 1]);
                 };
@@ -524,7 +527,7 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
                 }
 #pragma unroll 1
                 for (int b = 0; b < ((A.dbg & 1) ? 0 : (2 * FRY)); ++b) {
-                    const int y = FRY * rank + (b >> 1), z = 32 * (b & 1) + lane;
+                    const int y = FRY * rank + b_row(b), z = 32 * b_zh(b) + lane;
                     double2 v[8];
                     const double2 *R = rb + (b & 1) * FN * 32;
                     mbar_wait(&s_xbar[b & 1], (uint32_t)((b >> 1) & 1));
@@ -587,8 +590,30 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
                         tmem_ld16_nowait(ta, r);
 #endif
                         // taps ±m e in pairs (M2 is even): 8 independent loads per iteration
-#pragma unroll 1  // 8 loads in flight per tap pair; unrolling further measured slower
-                        for (int k = 0; k < ((A.dbg & 4) ? 0 : M2); k += 2) {
+                        int k0 = 0;
+                        // two tap pairs per iteration while 4 taps remain: 16 loads in flight
+#pragma unroll 1
+                        for (; k0 + 4 <= ((A.dbg & 4) ? 0 : M2); k0 += 4) {
+                            double2 a[4], c[4], a2[4], c2[4];
+                            const uint32_t b0 = swar_add(n[0], so[k0], H2), b1 = swar_add(n[0], so[k0 + 1], H2);
+                            const uint32_t b2 = swar_add(n[0], so[k0 + 2], H2), b3 = swar_add(n[0], so[k0 + 3], H2);
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                a[q] = ld2_nc_hint(fc + ((b0 + (uint32_t)q * 8u * FN2) & (uint32_t)(FNODES - 1)), keep);
+                                c[q] = ld2_nc_hint(fc + ((b1 + (uint32_t)q * 8u * FN2) & (uint32_t)(FNODES - 1)), keep);
+                            }
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                a2[q] = ld2_nc_hint(fc + ((b2 + (uint32_t)q * 8u * FN2) & (uint32_t)(FNODES - 1)), keep);
+                                c2[q] = ld2_nc_hint(fc + ((b3 + (uint32_t)q * 8u * FN2) & (uint32_t)(FNODES - 1)), keep);
+                            }
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) S[q] = add2(S[q], add2(a[q], c[q]));
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) S[q] = add2(S[q], add2(a2[q], c2[q]));
+                        }
+#pragma unroll 1
+                        for (int k = k0; k < ((A.dbg & 4) ? 0 : M2); k += 2) {
                             const uint32_t o0 = so[k], o1 = so[k + 1];
                             double2 a[4], c[4];
                             // the 4 nodes differ only in x (the top field, 8 q apart): one carry-less
@@ -754,6 +779,7 @@ dvm_status_t collide_fgain3d(dvm_plan_s *P, const double *f, int64_t f_stride, d
         for (int c = 1; c <= cmax; ++c) best = std::min(best, rounds(c));
         while (nchunks < cmax && rounds(nchunks) > best * 1.005) ++nchunks;
     }
+    if (P->tune.fg_chunks) nchunks = std::min(P->tune.fg_chunks, nloc);
     const int64_t items = npairs * nchunks;
     const int ngroups = (int)std::min<int64_t>(max_groups, items);
     Workspace &w = P->ws;

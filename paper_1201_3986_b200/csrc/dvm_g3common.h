@@ -45,14 +45,13 @@ __device__ __forceinline__ void role_wait(const unsigned int *ctrs, unsigned int
     role_sync(id);
 }
 
-// publish this CTA's role progress (all of the role's writes so far first)
+// publish this CTA's role progress: the role barrier orders every role thread's
+// writes before the leader's release store (release is cumulative; the CTA
+// barrier + one st/red.release pattern of grid barriers, no separate fence)
 __device__ __forceinline__ void role_signal(unsigned int *own, unsigned int value, bool leader, int id)
 {
     role_sync(id);
-    if (leader) {
-        __threadfence();
-        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(own), "r"(value) : "memory");
-    }
+    if (leader) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(own), "r"(value) : "memory");
 }
 
 // ---- tensor memory (TMEM) as the phase-B accumulator store: each B-role thread

@@ -150,6 +150,7 @@ struct Tuning {
     int fg_dbg = 0;      // k_fg2 timing bits: 1 skip B work, 2 skip A work, 4 skip taps (results wrong)
     int max_groups = 0;  // cap on concurrent cell groups of the persistent 3D kernels (0: all that fit)
     int ring_slots = 0;  // c5 kernel ring depth per group (0: 2)
+    int fg_chunks = 0;   // c5 kernel direction chunks per cell pair (0: automatic)
     int g3_cl = 0;       // frame-plane kernel CTAs per group at N = 32 (0: 8)
     int verbose = 0;     // launch geometry on stderr
 };

@@ -259,7 +259,8 @@ class Plan:
         _check(load().dvm_set_path(self._h, int(path)), "dvm_set_path")
 
     def set_tuning(self, key: str, value: int):
-        """dvm_set_tuning: "max_groups", "g3_cl", "verbose", "timing_dbg" (timing only: Q wrong)."""
+        """dvm_set_tuning: "max_groups", "ring_slots", "fg_chunks", "g3_cl", "verbose",
+        "timing_dbg" (timing only: Q wrong)."""
         _check(load().dvm_set_tuning(self._h, key.encode(), int(value)), "dvm_set_tuning")
 
     def set_weights(self, a_box=None, b_box=None):

@@ -800,12 +800,12 @@ def test_tile2d_path_matches_oracle(N, Nbar, Nt, cells, shard):
 def test_tuning_switches():
     """dvm_set_tuning: unknown keys and bad values are rejected (plan unchanged);
     timing_dbg changes Q (it skips work) and 0 restores the bitwise result;
-    max_groups / ring_slots change only the schedule (same operator to rounding)."""
+    max_groups / ring_slots / fg_chunks change only the schedule (same operator to rounding)."""
     from paper_1201_3986_b200 import DvmError
     f = dvm_inputs.make("c5", cells=4)
     p = _plan(3, 64, 8)
     q0 = _gpu(p, f)
-    for key, val in (("no_such_key", 1), ("ring_slots", 9), ("g3_cl", 3), ("timing_dbg", 99)):
+    for key, val in (("no_such_key", 1), ("ring_slots", 9), ("g3_cl", 3), ("timing_dbg", 99), ("fg_chunks", -1)):
         with pytest.raises(DvmError) as ei:
             p.set_tuning(key, val)
         assert ei.value.name == "DVM_E_STATE"
@@ -815,4 +815,7 @@ def test_tuning_switches():
     assert np.array_equal(_gpu(p, f), q0)
     p.set_tuning("max_groups", 1)
     p.set_tuning("ring_slots", 3)
+    np.testing.assert_allclose(_gpu(p, f), q0, rtol=0, atol=1e-12 * np.abs(q0).max())
+    p.set_tuning("max_groups", 0)
+    p.set_tuning("fg_chunks", 5)  # 2 pairs x 5 direction chunks on the 9 groups
     np.testing.assert_allclose(_gpu(p, f), q0, rtol=0, atol=1e-12 * np.abs(q0).max())
