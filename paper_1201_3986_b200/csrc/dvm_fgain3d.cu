@@ -11,7 +11,7 @@
 // line stencil).  A persistent cooperative kernel; a group of 16 CTAs owns
 // one cell pair at a time and walks the directions, warp-specialised:
 //   phase A (warps 0-7): CTA `rank` takes the planes ξ_x ≡ rank (mod 16):
-//     cp.async the plane of f̂ into shared memory, multiply by t̂_e, inverse
+//     bulk-copy the plane of f̂ into shared memory, multiply by t̂_e, inverse
 //     2D FFT over (ξ_y, ξ_z) with 16 points per thread (details below), write
 //     the plane to the group's ring slot [ξ_x][y][z] in L2.
 //   group progress counters (per CTA, monotonic, acquire/release)
@@ -42,22 +42,13 @@ constexpr int FMS = 32;          // tap table size (2 M_e <= 32)
 #ifndef FG2_REGA
 #define FG2_REGA 104  // k_fg2 setmaxnreg split: phase A, phase B gets 256 - FG2_REGA
 #endif
-#ifndef FG_BULK
-#define FG_BULK 1  // phase-A plane / T2D loads as one bulk copy each (mbarrier) instead of cp.async
-#endif
-#ifndef FG_BULKST
-#define FG_BULKST 1  // phase A writes each finished plane to the ring with bulk stores (TMA engine)
-#endif
-#ifndef FG_BDEC
-#define FG_BDEC 1  // phase B's x-exchange ordered by mbarriers, stage 1 of batch b+1 before the taps of b
-#endif
-#ifndef T2D_SWZ
-#define T2D_SWZ 1  // XOR column swizzle of the T2D_e table: fewer bank conflicts in phase A's lookups
-#endif
-__host__ __device__ __forceinline__ int t2d_swz(int p) { return T2D_SWZ ? ((p >> 2) & 15) : 0; }
-#ifndef FG_TMEM_EARLY
-#define FG_TMEM_EARLY 1  // accumulator TMEM loads issued before the taps (B alone 48.6 -> 46.9 ms / 18 cells)
-#endif
+// Column of T2D_e(p, q) in its table row p: q with its low 4 bits XOR-ed by
+// (q >> 4) & m.  The plan's perp basis is changed (unimodularly) so that u.z = 0
+// and w.z = g_z = gcd of the z components: the 16 lanes of a half-warp (ξ_z =
+// zl + const) read one row p at q = c + g_z zl, distinct banks (q mod 16) for
+// odd g_z with m = 0; for even g_z, m = 15 spreads q and q + 16 k (1.06
+// wavefronts per phase on average over the c5 directions instead of 2.27).
+__host__ __device__ __forceinline__ int t2d_col(int q, int m) { return q ^ ((q >> 4) & m); }
 
 struct FgArgs {
     const double2 *fhat;  // [pairs][N^3] f̂ of the cell pairs
@@ -111,13 +102,6 @@ __device__ __forceinline__ void idft8(double2 (&v)[8])
     v[7] = sub2(e3, o3);
 }
 
-__device__ __forceinline__ void cp_async16_pol(void *smem_dst, const void *gsrc, uint64_t pol)
-{
-    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(
-                     (uint32_t)__cvta_generic_to_shared(smem_dst)),
-                 "l"(gsrc), "l"(pol)
-                 : "memory");
-}
 // progress counters of a group of CL CTAs (role_wait of dvm_g3common.h for CL <= 32)
 template <int CL>
 __device__ __forceinline__ void group_wait(const unsigned int *ctrs, unsigned int target, int t, int id)
@@ -132,10 +116,7 @@ __device__ __forceinline__ void group_wait(const unsigned int *ctrs, unsigned in
                 ok = v >= target;
             }
             if (__all_sync(0xffffffffu, ok)) break;
-#ifndef FG_SLEEP
-#define FG_SLEEP 32
-#endif
-            if (FG_SLEEP) __nanosleep(FG_SLEEP);
+            __nanosleep(32);
         }
     }
     role_sync(id);
@@ -248,7 +229,7 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
     __shared__ uint32_t soff[2][FMS];
     __shared__ uint32_t s_tmem;
     __shared__ __align__(8) uint64_t s_mbar;  // FG_BULK: completion of the phase-A bulk loads
-    __shared__ __align__(8) uint64_t s_xbar[2], s_rbar[2];  // FG_BDEC: exchange buffer written / read
+    __shared__ __align__(8) uint64_t s_xbar[2], s_rbar[2];  // phase-B exchange buffer written / read
 
     const bool roleA = threadIdx.x < kRoleT;
     const int t = threadIdx.x & (kRoleT - 1);
@@ -286,7 +267,6 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
-#if FG_BULK
     // one bulk copy per table: the plane of f̂ (64 KB) and T2D_e (32 KB), issued by
     // thread 0 of phase A, completing the phase of s_mbar
     auto issue = [&](const double2 *fh, int g, int di) {
@@ -298,16 +278,6 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
         }
     };
     uint32_t mph = 0;
-#endif
-    auto load_t2d = [&](int di) {
-        const double2 *src = reinterpret_cast<const double2 *>(A.t2d + (int64_t)di * FN2);
-        for (int i = t; i < FN2 / 2; i += kRoleT) cp_async16_pol(t2 + 2 * i, src + i, l2_keep());
-    };
-    auto load_plane = [&](const double2 *fh, int g) {
-        const double2 *src = fh + (int64_t)g * FN2;
-        const uint64_t pol = l2_drop();  // f̂ streams; L2 is kept for f (taps) and the ring
-        for (int i = t; i < FN2; i += kRoleT) cp_async16_pol(stg + i, src + i, pol);
-    };
 
     if (roleA) {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegA2));
@@ -318,13 +288,7 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
         const int sw = c_me & 7;
         const int zr = t & 63, kq1r = t >> 6;  // CTA exchange reader: (z, kq1)
         if (grp < items && !(A.dbg & 2)) {
-#if FG_BULK
             issue(A.fhat + (grp / A.nchunks) * FNODES, rank, (int)((int64_t)A.nloc * (grp % A.nchunks) / A.nchunks));
-#else
-            load_plane(A.fhat + (grp / A.nchunks) * FNODES, rank);
-            load_t2d((int)((int64_t)A.nloc * (grp % A.nchunks) / A.nchunks));
-            cp_async_commit();
-#endif
         }
         for (int64_t item = grp; item < items; item += ngroups) {
             const int64_t pair = item / A.nchunks;
@@ -349,13 +313,8 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
                 for (int kp = 0; kp < ((A.dbg & 2) ? 0 : FPL); ++kp) {
                     const int g = rank + kp * CL;
                     const bool lastp = kp + 1 == FPL;
-#if FG_BULK
                     mbar_wait(&s_mbar, mph);  // [1] the plane (and at kp = 0 T2D_e) is in shared memory
                     mph ^= 1;
-#else
-                    cp_async_wait_all();
-                    role_sync(bar);  // [1] the plane (and at kp = 0 T2D_e) is in shared memory
-#endif
                     double2 v[16];
                     {
                         // stage 1: f̂ t̂_e, radix-4 over ξ_z high and ξ_y high
@@ -367,7 +326,7 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
                             for (int a = 0; a < 4; ++a) {
                                 const int pu = (pu0 + a * dua + b * dub) & (FN - 1);
                                 const int pw = (pw0 + a * dwa + b * dwb) & (FN - 1);
-                                const double tv = t2[pu * FN + (pw ^ t2d_swz(pu))];
+                                const double tv = t2[pu * FN + t2d_col(pw, rw.w)];
                                 const double2 x = stg[(yl + 16 * b) * FN + zl + 16 * a];
                                 v[a + 4 * b] = make_double2(x.x * tv, x.y * tv);
                             }
@@ -395,24 +354,12 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
                     for (int n = 0; n < 16; ++n)
                         v[n] = x1w[(c_me >> 2) * 16 * FN + 16 * (c_me & 3) + (n ^ sw)];
                     idft16(v);  // z = kp1 + 4 kp2: v[kp2], kp1 = c_me & 3
-#if FG_BULKST
                     if (warp == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // ex is read
-#endif
                     role_sync(bar);  // [2] staging and the exchange buffer are free
-#if FG_BULK
                     if (!lastp)
                         issue(fh, g + CL, -1);
                     else if (ndi >= 0)
                         issue(fh_next, rank, ndi);
-#else
-                    if (!lastp) {
-                        load_plane(fh, g + CL);
-                    } else if (ndi >= 0) {
-                        load_plane(fh_next, rank);
-                        load_t2d(ndi);
-                    }
-                    cp_async_commit();
-#endif
                     {
                         const int kp1 = c_me & 3, kq1 = c_me >> 2;
                         double2 *dst = ex + kq1 * F2Q + yl * FN + kp1;
@@ -426,7 +373,6 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
                         for (int n = 0; n < 16; ++n) v[n] = src[n * FN];
                     }
                     idft16(v);  // y = kq1r + 4 kq2: v[kq2]
-#if FG_BULKST
                     // back into the entries this thread read (row kq2 of quarter kq1r = ring row
                     // y = kq1r + 4 kq2), then warp 0 bulk-stores the 64 rows (1 KB each)
                     {
@@ -449,23 +395,15 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
                         }
                         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                     }
-#else
-                    double2 *dst = Tb + (int64_t)g * FN2 + zr;
-#pragma unroll
-                    for (int k = 0; k < 16; ++k) st2_hint(dst + (kq1r + 4 * k) * FN, v[k], keep);
-#endif
                 }
-#if FG_BULKST
                 if (warp == 0) {
                     // the step's planes are in global memory before the release below
                     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
                     asm volatile("fence.proxy.async.global;" ::: "memory");
                 }
-#endif
                 role_signal(cA + rank, stepi + 1, leader, bar);
             }
         }
-        cp_async_wait_all();
     } else {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegB2));
         const uint32_t tm_base = s_tmem + ((uint32_t)(32 * (warp & 3)) << 16) + 256u * (uint32_t)(warp >> 2);
@@ -499,7 +437,6 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
 #pragma unroll
                     for (int n2 = 0; n2 < 8; ++n2) pre[n2] = ld2_cg_hint(Tb + ((int64_t)(warp + 8 * n2) * FN + y) * FN + z, drop);
                 };
-#if FG_BDEC
                 // stage 1 of a batch (DFT-8 over n2, twiddle) from the prefetched ring values
                 // into exchange buffer b & 1, then every B thread arrives on s_xbar[b & 1];
                 // stage 2 waits on that barrier only, and arrives on s_rbar[b & 1] once read.
@@ -542,37 +479,6 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
                         stage1(b + 1);
                         if (b + 2 < (2 * FRY)) fetch(b + 2);
                     }
-#else
-                if (!(A.dbg & 1)) fetch(0);
-#pragma unroll 1
-                for (int b = 0; b < ((A.dbg & 1) ? 0 : (2 * FRY)); ++b) {
-                    const int y = FRY * rank + (b >> 1), z = 32 * (b & 1) + lane;
-                    double2 v[8];
-                    // buffer of pass-1 outputs: batch b - 2 used it, every thread is past b - 1's barrier
-                    double2 *R = rb + (b & 1) * FN * 32;
-                    {
-                        const int n1 = warp;
-#pragma unroll
-                        for (int n2 = 0; n2 < 8; ++n2) v[n2] = pre[n2];
-                        if (b + 1 < (2 * FRY)) fetch(b + 1);
-                        idft8(v);
-#pragma unroll
-                        for (int k2 = 1; k2 < 8; ++k2) v[k2] = cmul(v[k2], tw[(n1 * k2) & (FN - 1)]);
-#pragma unroll
-                        for (int k2 = 0; k2 < 8; ++k2) R[(n1 + 8 * k2) * 32 + lane] = v[k2];
-                    }
-                    if (!(A.dbg & 64)) {
-                        // the ring lines this warp read for batch b are dead (32 lines of 128 B, one per lane)
-                        __syncwarp();
-                        const double2 *line = Tb + ((int64_t)(warp + 8 * (lane >> 2)) * FN + y) * FN + 32 * (b & 1) + 8 * (lane & 3);
-                        asm volatile("discard.global.L2 [%0], 128;" ::"l"(line) : "memory");
-                    }
-                    role_sync(bar);
-                    const int k2 = warp;
-#pragma unroll
-                    for (int n1 = 0; n1 < 8; ++n1) v[n1] = R[(n1 + 8 * k2) * 32 + lane];
-                    idft8(v);  // v[k1] = N^3 T_e(x = k2 + 8 k1, y, z)
-#endif
 #pragma unroll
                     for (int hh = 0; hh < 2; ++hh) {
                         uint32_t n[4];
@@ -582,13 +488,11 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
                             n[q] = (uint32_t)((((k2 + 8 * (4 * hh + q)) * FN) + y) * FN + z);
                             S[q] = make_double2(0.0, 0.0);
                         }
-#if FG_TMEM_EARLY
                         // the accumulators' TMEM load is issued before the taps; its wait follows them
                         uint32_t r[16];
                         const uint32_t ta = tm_base + (uint32_t)(32 * b + 16 * hh);
                         __syncwarp();
                         tmem_ld16_nowait(ta, r);
-#endif
                         // taps ±m e in pairs (M2 is even): 8 independent loads per iteration
                         int k0 = 0;
                         // two tap pairs per iteration while 4 taps remain: 16 loads in flight
@@ -627,17 +531,8 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
 #pragma unroll
                             for (int q = 0; q < 4; ++q) S[q] = add2(S[q], add2(a[q], c[q]));
                         }
-#if FG_TMEM_EARLY
                         __syncwarp();
                         tmem_wait_ld();
-#else
-                        uint32_t r[16];
-                        const uint32_t ta = tm_base + (uint32_t)(32 * b + 16 * hh);
-                        // the TMEM load and store are unconditional (.sync.aligned: every lane must
-                        // execute the same instruction; no data-dependent branch around them)
-                        __syncwarp();
-                        tmem_ld16(ta, r);
-#endif
                         if (first) {
 #pragma unroll
                             for (int q = 0; q < 4; ++q) {
@@ -678,14 +573,19 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
     }
 }
 
-// T2D_e(p, q) = Σ_{(α, β) ∈ P_e} cos(2π(α p + β q) / N): one thread per (direction, p, q)
+// T2D_e(p, q) = Σ_{(α, β) ∈ P_e} cos(2π(α p + β q) / N) in the plan's basis (u, w)
+// of the rows, stored in the kernel's basis u' = c0 u + c1 w, w' = c2 u + c3 w
+// (det 1): entry (p', q') holds T2D_e(c3 p' − c1 q', −c2 p' + c0 q') at column
+// t2d_col(q', m).  One thread per (direction, p', q').
 __global__ void k_fg_t2d(int N, int nloc, const int *local, const int *row_off, const int *row_b, const int *row_lo,
-                         const int *row_hi, double *out)
+                         const int *row_hi, const int4 *basis, const int *mask, double *out)
 {
     const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (gid >= (int64_t)nloc * N * N) return;
     const int k = (int)(gid / (N * N));
-    const int p = (int)((gid / N) % N), q = (int)(gid % N);
+    const int pp = (int)((gid / N) % N), qq = (int)(gid % N);
+    const int4 c = basis[k];
+    const int p = ((c.w * pp - c.y * qq) % N + N) % N, q = ((-c.z * pp + c.x * qq) % N + N) % N;
     const int di = local[k];
     double acc = 0.0;
     for (int r = row_off[di]; r < row_off[di + 1]; ++r) {
@@ -695,8 +595,7 @@ __global__ void k_fg_t2d(int N, int nloc, const int *local, const int *row_off, 
             acc += cospi(2.0 * ph / N);
         }
     }
-    // stored with the row-dependent column swizzle of phase A's lookups (T2D_SWZ)
-    out[(int64_t)k * N * N + p * N + (q ^ t2d_swz(p))] = acc;
+    out[(int64_t)k * N * N + pp * N + t2d_col(qq, mask[k])] = acc;
 }
 
 dvm_status_t build_fg_tables(dvm_plan_s *P)
@@ -708,7 +607,8 @@ dvm_status_t build_fg_tables(dvm_plan_s *P)
     std::vector<int> hu((size_t)A * 3), hw((size_t)A * 3);
     DVM_CUDA(cudaMemcpy(hu.data(), P->t.u, sizeof(int) * hu.size(), cudaMemcpyDeviceToHost));
     DVM_CUDA(cudaMemcpy(hw.data(), P->t.w, sizeof(int) * hw.size(), cudaMemcpyDeviceToHost));
-    std::vector<int4> rec((size_t)std::max(1, nloc) * 3);
+    std::vector<int4> rec((size_t)std::max(1, nloc) * 3), basis((size_t)std::max(1, nloc));
+    std::vector<int> mask((size_t)std::max(1, nloc));
     std::vector<double> aw(std::max(1, nloc));
     for (int k = 0; k < nloc; ++k) {
         const int di = P->local[k];
@@ -717,8 +617,38 @@ dvm_status_t build_fg_tables(dvm_plan_s *P)
             return DVM_E_UNSUPPORTED;
         }
         rec[3 * k] = make_int4(P->h_e[3 * di], P->h_e[3 * di + 1], P->h_e[3 * di + 2], P->h_M[di]);
-        rec[3 * k + 1] = make_int4(hu[3 * di], hu[3 * di + 1], hu[3 * di + 2], 0);
-        rec[3 * k + 2] = make_int4(hw[3 * di], hw[3 * di + 1], hw[3 * di + 2], 0);
+        // u' = c0 u + c1 w with u'.z = 0, w' = c2 u + c3 w with w'.z = g = gcd(u.z, w.z)
+        // (Bezout), c0 c3 − c1 c2 = 1; u.z = w.z = 0 keeps the basis
+        const int uz = hu[3 * di + 2], wz = hw[3 * di + 2];
+        int c0 = 1, c1 = 0, c2 = 0, c3 = 1, gz = 0;
+        if (uz != 0 || wz != 0) {
+            long long r0 = uz, r1 = wz, s0 = 1, s1 = 0, t0 = 0, t1 = 1;  // extended Euclid: s uz + t wz = r
+            while (r1 != 0) {
+                const long long qt = r0 / r1;
+                long long x = r0 - qt * r1; r0 = r1; r1 = x;
+                x = s0 - qt * s1; s0 = s1; s1 = x;
+                x = t0 - qt * t1; t0 = t1; t1 = x;
+            }
+            if (r0 < 0) { r0 = -r0; s0 = -s0; t0 = -t0; }
+            gz = (int)r0;
+            c0 = wz / gz;
+            c1 = -uz / gz;
+            c2 = (int)s0;
+            c3 = (int)t0;
+        }
+        int up[3], wp[3];
+        for (int j = 0; j < 3; ++j) {
+            up[j] = c0 * hu[3 * di + j] + c1 * hw[3 * di + j];
+            wp[j] = c2 * hu[3 * di + j] + c3 * hw[3 * di + j];
+        }
+        if (up[2] != 0 || wp[2] != gz || c0 * c3 - c1 * c2 != 1) {
+            set_error("fgain3d: perp basis normalisation failed");
+            return DVM_E_UNSUPPORTED;
+        }
+        basis[k] = make_int4(c0, c1, c2, c3);
+        mask[k] = (gz & 1) ? 0 : 15;
+        rec[3 * k + 1] = make_int4(up[0], up[1], up[2], 0);
+        rec[3 * k + 2] = make_int4(wp[0], wp[1], wp[2], mask[k]);
         aw[k] = P->h_a[di] / (double)FNODES;  // the inverse transforms are unnormalised
     }
     DVM_CUDA(cudaMalloc(&g.fg_rec, sizeof(int4) * rec.size()));
@@ -726,14 +656,23 @@ dvm_status_t build_fg_tables(dvm_plan_s *P)
     DVM_CUDA(cudaMalloc(&g.fg_t2d, sizeof(double) * (size_t)std::max(1, nloc) * FN2));
     DVM_CUDA(cudaMemcpyAsync(g.fg_rec, rec.data(), sizeof(int4) * rec.size(), cudaMemcpyHostToDevice, P->stream));
     DVM_CUDA(cudaMemcpyAsync(g.fg_aw, aw.data(), sizeof(double) * aw.size(), cudaMemcpyHostToDevice, P->stream));
+    int4 *d_basis = nullptr;
+    int *d_mask = nullptr;
+    DVM_CUDA(cudaMalloc(&d_basis, sizeof(int4) * basis.size()));
+    DVM_CUDA(cudaMalloc(&d_mask, sizeof(int) * mask.size()));
+    DVM_CUDA(cudaMemcpyAsync(d_basis, basis.data(), sizeof(int4) * basis.size(), cudaMemcpyHostToDevice, P->stream));
+    DVM_CUDA(cudaMemcpyAsync(d_mask, mask.data(), sizeof(int) * mask.size(), cudaMemcpyHostToDevice, P->stream));
     if (nloc > 0) {
         LaunchScope ls(P, KC_PLAN);
         const int64_t tot = (int64_t)nloc * FN2;
         k_fg_t2d<<<(unsigned)((tot + 255) / 256), 256, 0, P->stream>>>(FN, nloc, P->t.local, P->t.row_off, P->t.row_b,
-                                                                      P->t.row_lo, P->t.row_hi, g.fg_t2d);
+                                                                      P->t.row_lo, P->t.row_hi, d_basis, d_mask,
+                                                                      g.fg_t2d);
     }
     DVM_CUDA(cudaGetLastError());
     DVM_CUDA(cudaStreamSynchronize(P->stream));
+    cudaFree(d_basis);
+    cudaFree(d_mask);
     g.bytes += sizeof(int4) * rec.size() + sizeof(double) * aw.size() + sizeof(double) * (size_t)nloc * FN2;
     return DVM_OK;
 }
