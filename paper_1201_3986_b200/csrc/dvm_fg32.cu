@@ -5,12 +5,14 @@
 // filters are real and even, f is real):
 //   T_a + i T_b = IFFT( f̂ (t̂_a + i t̂_b) ),   t̂_e(ξ) = T2D_e(u.ξ mod N, w.ξ mod N)
 // (the paper's spectral evaluation of the α'_p factor, PAPER.md:561-570,
-// 816-819; reading R23).  All A/2 pair arrays are formed at once (k_f32_mult),
-// transformed by the batched inverse passes of dvm_loss.cu (3 launches for the
-// whole batch, L2-resident: A/2 × 512 KB, 74 MB for c4), then one kernel adds
-// a_e S_e T_e for every node and direction chunk with S_e = Σ_{1<=|m|<=M_e}
-// f(.+me) read as taps, and the chunk partials are summed in
-// chunk order on top of −fΛ (the loss, one FFT convolution, reading R21).
+// 816-819; reading R23).  k_f32_plane forms each plane ξ_0 of every pair
+// product (T2D lookups in the basis of perp_basis_zfree: a warp reads one
+// table row) and runs the inverse 2D DFT over (ξ_1, ξ_2) into
+// Z[pair][ξ_0][y][z] (A/2 × 512 KB, 74 MB for c4, L2-resident); k_f32_xgain
+// runs the inverse DFT along ξ_0 for one row y and a chunk of pairs, then adds
+// a_e S_e T_e for its nodes with S_e = Σ_{1<=|m|<=M_e} f(.+me) read as taps
+// (PAPER.md:817); the chunk partials are summed in chunk order on top of −fΛ
+// (the loss, one FFT convolution through the same plane kernel, reading R21).
 // Deterministic: fixed summation order everywhere.
 #include <math.h>
 
@@ -26,13 +28,18 @@ constexpr int K32 = 32;
 constexpr int K32N = K32 * K32 * K32;
 constexpr int K32CHUNKS = 32;  // direction-pair chunks of the gain kernel (partials summed in order)
 
-// T2D_e(p, q) = Σ_{(α, β) ∈ P_e} cos(2π(α p + β q) / N), one thread per (direction, p, q)
+// T2D_e(p, q) = Σ_{(α, β) ∈ P_e} cos(2π(α p + β q) / N) in the plan's basis (u, w),
+// stored in the basis of perp_basis_zfree (u' = c0 u + c1 w, w' = c2 u + c3 w):
+// entry (p', q') holds T2D_e(c3 p' − c1 q', −c2 p' + c0 q') at column
+// t2d_col(q', m) of row p'.  One thread per (direction, p', q').
 __global__ void k_f32_t2d(int nloc, const int *local, const int *row_off, const int *row_b, const int *row_lo,
-                          const int *row_hi, double *out)
+                          const int *row_hi, const int4 *basis, const int *mask, double *out)
 {
     const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (gid >= (int64_t)nloc * K32 * K32) return;
-    const int k = (int)(gid / (K32 * K32)), p = (int)((gid / K32) % K32), q = (int)(gid % K32);
+    const int k = (int)(gid / (K32 * K32)), pp = (int)((gid / K32) % K32), qq = (int)(gid % K32);
+    const int4 cb = basis[k];
+    const int p = ((cb.w * pp - cb.y * qq) % K32 + K32) % K32, q = ((-cb.z * pp + cb.x * qq) % K32 + K32) % K32;
     const int di = local[k];
     double acc = 0.0;
     for (int r = row_off[di]; r < row_off[di + 1]; ++r)
@@ -40,7 +47,7 @@ __global__ void k_f32_t2d(int nloc, const int *local, const int *row_off, const 
             const int ph = ((a * p + row_b[r] * q) % K32 + K32) % K32;
             acc += cospi(2.0 * ph / K32);
         }
-    out[gid] = acc;
+    out[(int64_t)k * K32 * K32 + pp * K32 + t2d_col(qq, mask[k])] = acc;
 }
 
 constexpr int P32 = K32 + 1;  // padded pitch of a 32 x 32 tile in shared memory (double2)
@@ -82,11 +89,11 @@ __device__ __forceinline__ void idft8_(double2 (&v)[8])
 
 // Inverse 32-point DFTs of the 32 lines of a 32 x 32 tile in shared memory, in
 // place: element n of line l at buf[l * ls + n * es].  128 threads: thread
-// (l = t >> 2, j = t & 3) takes n = j + 4 q (q < 8): DFT-8 over q -> k1,
+// (l = t & 31, j = t >> 5) takes n = j + 4 q (q < 8): DFT-8 over q -> k1,
 // × ω32^{j k1}, then DFT-4 over j for k1 = 2 j', 2 j' + 1 -> k = k1 + 8 k2.
 __device__ __forceinline__ void ifft32_lines(double2 *buf, int ls, int es, const double2 *tw32)
 {
-    const int t = threadIdx.x, l = t >> 2, j = t & 3;
+    const int t = threadIdx.x, l = t & 31, j = t >> 5;  // 8 lanes of a phase: 8 lines, distinct banks
     double2 v[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) v[q] = buf[l * ls + (j + 4 * q) * es];
@@ -150,9 +157,11 @@ __global__ void __launch_bounds__(128) k_f32_plane(const double2 *__restrict__ f
     const double *Ta = t2d + (int64_t)ka * K32 * K32, *Tb = t2d + (int64_t)(hb ? kb : ka) * K32 * K32;
     for (int i = t; i < K32 * K32; i += 128) {
         const int x1 = i >> 5, x2 = i & 31;
-        const double ta = Ta[((ua.x * x0 + ua.y * x1 + ua.z * x2) & 31) * K32 + ((wa.x * x0 + wa.y * x1 + wa.z * x2) & 31)];
+        // a warp steps ξ_2 = x2: one row of each table (u'.z = 0), 2 lines per lookup
+        const double ta = Ta[((ua.x * x0 + ua.y * x1 + ua.z * x2) & 31) * K32 +
+                                  t2d_col((wa.x * x0 + wa.y * x1 + wa.z * x2) & 31, wa.w)];
         const double tb = hb ? Tb[((ub.x * x0 + ub.y * x1 + ub.z * x2) & 31) * K32 +
-                                  ((wb.x * x0 + wb.y * x1 + wb.z * x2) & 31)]
+                                       t2d_col((wb.x * x0 + wb.y * x1 + wb.z * x2) & 31, wb.w)]
                              : 0.0;
         const double2 fh = fhat[x0 * K32 * K32 + i];
         buf[x1 * P32 + x2] = make_double2(fh.x * ta - fh.y * tb, fh.x * tb + fh.y * ta);
@@ -273,13 +282,21 @@ dvm_status_t build_f32_tables(dvm_plan_s *P)
     DVM_CUDA(cudaMemcpy(hw.data(), P->t.w, sizeof(int) * hw.size(), cudaMemcpyDeviceToHost));
     int mmax = 1;
     for (int di : P->local) mmax = std::max(mmax, P->h_M[di]);
-    std::vector<int4> rec((size_t)std::max(1, 2 * nloc));
+    std::vector<int4> rec((size_t)std::max(1, 2 * nloc)), basis((size_t)std::max(1, nloc));
+    std::vector<int> mask((size_t)std::max(1, nloc));
     std::vector<uint32_t> off((size_t)std::max(1, nloc) * 2 * mmax, 0u);
     std::vector<double> aw(std::max(1, nloc));
     for (int k = 0; k < nloc; ++k) {
         const int di = P->local[k];
-        rec[k] = make_int4(hu[3 * di], hu[3 * di + 1], hu[3 * di + 2], P->h_M[di]);
-        rec[nloc + k] = make_int4(hw[3 * di], hw[3 * di + 1], hw[3 * di + 2], 0);
+        int c[4], up[3], wp[3], gz = 0;
+        if (!perp_basis_zfree(&hu[3 * di], &hw[3 * di], c, up, wp, &gz)) {
+            set_error("fg32: perp basis normalisation failed");
+            return DVM_E_UNSUPPORTED;
+        }
+        basis[k] = make_int4(c[0], c[1], c[2], c[3]);
+        mask[k] = (gz & 1) ? 0 : 15;
+        rec[k] = make_int4(up[0], up[1], up[2], P->h_M[di]);
+        rec[nloc + k] = make_int4(wp[0], wp[1], wp[2], mask[k]);
         for (int m = 1; m <= P->h_M[di]; ++m)
             for (int sg = 0; sg < 2; ++sg) {
                 int c[3];
@@ -295,14 +312,23 @@ dvm_status_t build_f32_tables(dvm_plan_s *P)
     DVM_CUDA(cudaMemcpyAsync(g.f32_rec, rec.data(), sizeof(int4) * rec.size(), cudaMemcpyHostToDevice, P->stream));
     DVM_CUDA(cudaMemcpyAsync(g.f32_off, off.data(), sizeof(uint32_t) * off.size(), cudaMemcpyHostToDevice, P->stream));
     DVM_CUDA(cudaMemcpyAsync(g.f32_aw, aw.data(), sizeof(double) * aw.size(), cudaMemcpyHostToDevice, P->stream));
+    int4 *d_basis = nullptr;
+    int *d_mask = nullptr;
+    DVM_CUDA(cudaMalloc(&d_basis, sizeof(int4) * basis.size()));
+    DVM_CUDA(cudaMalloc(&d_mask, sizeof(int) * mask.size()));
+    DVM_CUDA(cudaMemcpyAsync(d_basis, basis.data(), sizeof(int4) * basis.size(), cudaMemcpyHostToDevice, P->stream));
+    DVM_CUDA(cudaMemcpyAsync(d_mask, mask.data(), sizeof(int) * mask.size(), cudaMemcpyHostToDevice, P->stream));
     if (nloc > 0) {
         LaunchScope ls(P, KC_PLAN);
         const int64_t tot = (int64_t)nloc * K32 * K32;
         k_f32_t2d<<<(unsigned)((tot + 255) / 256), 256, 0, P->stream>>>(nloc, P->t.local, P->t.row_off, P->t.row_b,
-                                                                       P->t.row_lo, P->t.row_hi, g.f32_t2d);
+                                                                       P->t.row_lo, P->t.row_hi, d_basis, d_mask,
+                                                                       g.f32_t2d);
     }
     DVM_CUDA(cudaGetLastError());
     DVM_CUDA(cudaStreamSynchronize(P->stream));
+    cudaFree(d_basis);
+    cudaFree(d_mask);
     g.f32_mmax = mmax;
     g.bytes += sizeof(int4) * rec.size() + sizeof(uint32_t) * off.size() + sizeof(double) * aw.size() +
                sizeof(double) * (size_t)nloc * K32 * K32;

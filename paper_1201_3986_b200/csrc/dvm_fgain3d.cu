@@ -42,13 +42,10 @@ constexpr int FMS = 32;          // tap table size (2 M_e <= 32)
 #ifndef FG2_REGA
 #define FG2_REGA 104  // k_fg2 setmaxnreg split: phase A, phase B gets 256 - FG2_REGA
 #endif
-// Column of T2D_e(p, q) in its table row p: q with its low 4 bits XOR-ed by
-// (q >> 4) & m.  The plan's perp basis is changed (unimodularly) so that u.z = 0
-// and w.z = g_z = gcd of the z components: the 16 lanes of a half-warp (ξ_z =
-// zl + const) read one row p at q = c + g_z zl, distinct banks (q mod 16) for
-// odd g_z with m = 0; for even g_z, m = 15 spreads q and q + 16 k (1.06
-// wavefronts per phase on average over the c5 directions instead of 2.27).
-__host__ __device__ __forceinline__ int t2d_col(int q, int m) { return q ^ ((q >> 4) & m); }
+// T2D_e lookups of phase A: a half-warp (ξ_z = zl + const) reads one table row
+// at q = c + g_z zl in the basis of perp_basis_zfree (dvm_internal.h): distinct
+// banks for odd g_z, the t2d_col swizzle for even g_z (1.06 wavefronts per phase
+// on average over the c5 directions instead of 2.27 in the plan's basis).
 
 struct FgArgs {
     const double2 *fhat;  // [pairs][N^3] f̂ of the cell pairs
@@ -617,34 +614,12 @@ dvm_status_t build_fg_tables(dvm_plan_s *P)
             return DVM_E_UNSUPPORTED;
         }
         rec[3 * k] = make_int4(P->h_e[3 * di], P->h_e[3 * di + 1], P->h_e[3 * di + 2], P->h_M[di]);
-        // u' = c0 u + c1 w with u'.z = 0, w' = c2 u + c3 w with w'.z = g = gcd(u.z, w.z)
-        // (Bezout), c0 c3 − c1 c2 = 1; u.z = w.z = 0 keeps the basis
-        const int uz = hu[3 * di + 2], wz = hw[3 * di + 2];
-        int c0 = 1, c1 = 0, c2 = 0, c3 = 1, gz = 0;
-        if (uz != 0 || wz != 0) {
-            long long r0 = uz, r1 = wz, s0 = 1, s1 = 0, t0 = 0, t1 = 1;  // extended Euclid: s uz + t wz = r
-            while (r1 != 0) {
-                const long long qt = r0 / r1;
-                long long x = r0 - qt * r1; r0 = r1; r1 = x;
-                x = s0 - qt * s1; s0 = s1; s1 = x;
-                x = t0 - qt * t1; t0 = t1; t1 = x;
-            }
-            if (r0 < 0) { r0 = -r0; s0 = -s0; t0 = -t0; }
-            gz = (int)r0;
-            c0 = wz / gz;
-            c1 = -uz / gz;
-            c2 = (int)s0;
-            c3 = (int)t0;
-        }
-        int up[3], wp[3];
-        for (int j = 0; j < 3; ++j) {
-            up[j] = c0 * hu[3 * di + j] + c1 * hw[3 * di + j];
-            wp[j] = c2 * hu[3 * di + j] + c3 * hw[3 * di + j];
-        }
-        if (up[2] != 0 || wp[2] != gz || c0 * c3 - c1 * c2 != 1) {
+        int c[4], up[3], wp[3], gz = 0;
+        if (!perp_basis_zfree(&hu[3 * di], &hw[3 * di], c, up, wp, &gz)) {
             set_error("fgain3d: perp basis normalisation failed");
             return DVM_E_UNSUPPORTED;
         }
+        const int c0 = c[0], c1 = c[1], c2 = c[2], c3 = c[3];
         basis[k] = make_int4(c0, c1, c2, c3);
         mask[k] = (gz & 1) ? 0 : 15;
         rec[3 * k + 1] = make_int4(up[0], up[1], up[2], 0);

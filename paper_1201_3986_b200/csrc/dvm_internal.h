@@ -28,6 +28,42 @@ __host__ __device__ inline uint32_t swar_add(uint32_t a, uint32_t b, uint32_t H)
     return ((a & ~H) + (b & ~H)) ^ ((a ^ b) & H);
 }
 
+// Perp-basis change for the T2D_e table lookups of the 3D FFT gain kernels:
+// u' = c[0] u + c[1] w, w' = c[2] u + c[3] w with c[0] c[3] − c[1] c[2] = 1,
+// u'.z = 0 and w'.z = g = gcd(u.z, w.z) (extended Euclid; u.z = w.z = 0 keeps
+// the basis, g = 0).  Lanes that step ξ_z then read one table row at columns
+// q0 + g·lane: distinct banks for odd g; the column swizzle t2d_col below with
+// mask (g odd ? 0 : 15) spreads even g.  Returns false if the result fails its
+// own check.
+inline bool perp_basis_zfree(const int *u, const int *w, int c[4], int up[3], int wp[3], int *g)
+{
+    const int uz = u[2], wz = w[2];
+    c[0] = 1, c[1] = 0, c[2] = 0, c[3] = 1;
+    *g = 0;
+    if (uz != 0 || wz != 0) {
+        long long r0 = uz, r1 = wz, s0 = 1, s1 = 0, t0 = 0, t1 = 1;  // s uz + t wz = r
+        while (r1 != 0) {
+            const long long q = r0 / r1;
+            long long x = r0 - q * r1;
+            r0 = r1, r1 = x;
+            x = s0 - q * s1;
+            s0 = s1, s1 = x;
+            x = t0 - q * t1;
+            t0 = t1, t1 = x;
+        }
+        if (r0 < 0) r0 = -r0, s0 = -s0, t0 = -t0;
+        *g = (int)r0;
+        c[0] = wz / *g, c[1] = -uz / *g, c[2] = (int)s0, c[3] = (int)t0;
+    }
+    for (int j = 0; j < 3; ++j) {
+        up[j] = c[0] * u[j] + c[1] * w[j];
+        wp[j] = c[2] * u[j] + c[3] * w[j];
+    }
+    return up[2] == 0 && wp[2] == *g && c[0] * c[3] - c[1] * c[2] == 1;
+}
+// column of T2D'(p, q) in its table row (see perp_basis_zfree)
+__host__ __device__ __forceinline__ int t2d_col(int q, int m) { return q ^ ((q >> 4) & m); }
+
 __host__ __device__ inline uint32_t pack_vec(const int *c, int d, int p, int N)
 {
     uint32_t r = 0;

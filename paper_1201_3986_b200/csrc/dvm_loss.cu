@@ -59,16 +59,16 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b)
 #define FFT_B256 1
 #endif
 // lines per CTA (the kernel's tile and the launcher's grid): 16 KB tiles, but fewer
-// lines for N = 256 (a 2D cell has only 256 lines: more CTAs per pass)
+// lines for N = 256 (a 2D cell has only 256 lines: more CTAs per pass), and 4
+// lines when the default tiling gives fewer CTAs than SMs (fft_pass)
 __host__ __device__ constexpr int fft_lines_per_cta(int N)
 {
     return N == 256 ? FFT_B256 : ((1024 / N) < N ? (1024 / N) : N);
 }
 
-template <int N>
+template <int N, int B>
 __global__ void __launch_bounds__(kFT) k_fft_pass(FftArgs A)
 {
-    constexpr int B = fft_lines_per_cta(N);
     constexpr int LOGN = N == 16 ? 4 : N == 32 ? 5 : N == 64 ? 6 : N == 128 ? 7 : 8;
     __shared__ double2 buf[B * N];
     const int d = A.d, ax = A.ax;
@@ -275,11 +275,15 @@ template <int N>
 dvm_status_t fft_pass(dvm_plan_s *P, const FftArgs &a)
 {
     constexpr int B = fft_lines_per_cta(N);
+    constexpr int BS = B < 4 ? B : 4;  // small batches (a single cell at N <= 64): 4 lines per CTA, more CTAs
     int64_t nodes = 1;
     for (int j = 0; j < a.d; ++j) nodes *= N;
     const int64_t tiles = a.npairs * (nodes / N / B);
     LaunchScope ls(P, KC_FFT);
-    k_fft_pass<N><<<(unsigned)tiles, kFT, 0, P->stream>>>(a);
+    if (tiles < 148)
+        k_fft_pass<N, BS><<<(unsigned)(a.npairs * (nodes / N / BS)), kFT, 0, P->stream>>>(a);
+    else
+        k_fft_pass<N, B><<<(unsigned)tiles, kFT, 0, P->stream>>>(a);
     DVM_CUDA(cudaGetLastError());
     return DVM_OK;
 }
