@@ -11,7 +11,7 @@
 //               runs forward, × λ̂ and inverse in shared memory, d − 1
 //               inverse (the last writes −f Λ)
 // k_fft_pass is a radix-2 fp64 pass along one axis over tiles of lines in
-// shared memory, twiddles exp(−2πik/N) from sincospi.
+// shared memory (two stages per barrier), twiddles exp(−2πik/N) from sincospi.
 #include <math.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -71,6 +71,8 @@ __global__ void __launch_bounds__(kFT) k_fft_pass(FftArgs A)
 {
     constexpr int LOGN = N == 16 ? 4 : N == 32 ? 5 : N == 64 ? 6 : N == 128 ? 7 : 8;
     __shared__ double2 buf[B * N];
+    __shared__ double2 stw[N / 2];
+    for (int k = threadIdx.x; k < N / 2; k += kFT) stw[k] = A.tw[k];
     const int d = A.d, ax = A.ax;
     int64_t nodes = 1;
     for (int j = 0; j < d; ++j) nodes *= N;
@@ -110,17 +112,45 @@ __global__ void __launch_bounds__(kFT) k_fft_pass(FftArgs A)
         buf[i * N + tr] = v;
     }
     __syncthreads();
+    // radix-2 DIT stages, two per barrier: a thread takes the 4 elements
+    // i0 + {0, 1, 2, 3} half of one 4-half block and applies stage `half` and
+    // stage `2 half` to them in registers (the same butterflies and twiddles
+    // as one stage at a time)
     auto stages = [&](bool inverse) {
-        for (int half = 1; half < N; half <<= 1) {
+        auto bfly = [](double2 u, double2 x, double2 w, double2 &lo, double2 &hi) {
+            const double2 v = cmul(x, w);
+            lo = make_double2(u.x + v.x, u.y + v.y);
+            hi = make_double2(u.x - v.x, u.y - v.y);
+        };
+        int half = 1;
+        for (; 4 * half <= N; half <<= 2) {
+            for (int b = threadIdx.x; b < B * N / 4; b += kFT) {
+                const int i = b / (N / 4), k = b % (N / 4);
+                const int pos = k % half, grp = k / half;
+                const int i0 = grp * 4 * half + pos;
+                double2 w1 = stw[pos * (N / (2 * half))];
+                double2 wa = stw[pos * (N / (4 * half))], wb = stw[(pos + half) * (N / (4 * half))];
+                if (inverse) w1.y = -w1.y, wa.y = -wa.y, wb.y = -wb.y;
+                double2 *r = buf + i * N + i0;
+                double2 y0, y1, y2, y3, z0, z1, z2, z3;
+                bfly(r[0], r[half], w1, y0, y1);
+                bfly(r[2 * half], r[3 * half], w1, y2, y3);
+                bfly(y0, y2, wa, z0, z2);
+                bfly(y1, y3, wb, z1, z3);
+                r[0] = z0, r[half] = z1, r[2 * half] = z2, r[3 * half] = z3;
+            }
+            __syncthreads();
+        }
+        if (half < N) {  // log2 N odd: the last stage alone
             for (int b = threadIdx.x; b < B * N / 2; b += kFT) {
                 const int i = b / (N / 2), k = b % (N / 2);
                 const int pos = k & (half - 1), grp = k / half;
                 const int i0 = grp * 2 * half + pos, i1 = i0 + half;
-                double2 w = A.tw[pos * (N / (2 * half))];
+                double2 w = stw[pos * (N / (2 * half))];
                 if (inverse) w.y = -w.y;
-                const double2 u = buf[i * N + i0], v = cmul(buf[i * N + i1], w);
-                buf[i * N + i0] = make_double2(u.x + v.x, u.y + v.y);
-                buf[i * N + i1] = make_double2(u.x - v.x, u.y - v.y);
+                double2 lo, hi;
+                bfly(buf[i * N + i0], buf[i * N + i1], w, lo, hi);
+                buf[i * N + i0] = lo, buf[i * N + i1] = hi;
             }
             __syncthreads();
         }
