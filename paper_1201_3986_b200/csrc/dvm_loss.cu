@@ -52,6 +52,54 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b)
     return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
 
+// Radix-2 DIT stages over LINES lines of N points in shared memory (input in
+// bit-reversed order, output natural), two stages per barrier: a thread takes
+// the 4 elements i0 + {0, 1, 2, 3} half of one 4-half block and applies stage
+// `half` and stage `2 half` in registers (the same butterflies and twiddles as
+// one stage at a time).  Every thread of the block calls it; it ends with a
+// barrier.
+template <int N, int LINES>
+__device__ __forceinline__ void fft_stages(double2 *buf, const double2 *stw, bool inverse)
+{
+    auto bfly = [](double2 u, double2 x, double2 w, double2 &lo, double2 &hi) {
+        const double2 v = cmul(x, w);
+        lo = make_double2(u.x + v.x, u.y + v.y);
+        hi = make_double2(u.x - v.x, u.y - v.y);
+    };
+    int half = 1;
+    for (; 4 * half <= N; half <<= 2) {
+        for (int b = threadIdx.x; b < LINES * N / 4; b += blockDim.x) {
+            const int i = b / (N / 4), k = b % (N / 4);
+            const int pos = k % half, grp = k / half;
+            const int i0 = grp * 4 * half + pos;
+            double2 w1 = stw[pos * (N / (2 * half))];
+            double2 wa = stw[pos * (N / (4 * half))], wb = stw[(pos + half) * (N / (4 * half))];
+            if (inverse) w1.y = -w1.y, wa.y = -wa.y, wb.y = -wb.y;
+            double2 *r = buf + i * N + i0;
+            double2 y0, y1, y2, y3, z0, z1, z2, z3;
+            bfly(r[0], r[half], w1, y0, y1);
+            bfly(r[2 * half], r[3 * half], w1, y2, y3);
+            bfly(y0, y2, wa, z0, z2);
+            bfly(y1, y3, wb, z1, z3);
+            r[0] = z0, r[half] = z1, r[2 * half] = z2, r[3 * half] = z3;
+        }
+        __syncthreads();
+    }
+    if (half < N) {  // log2 N odd: the last stage alone
+        for (int b = threadIdx.x; b < LINES * N / 2; b += blockDim.x) {
+            const int i = b / (N / 2), k = b % (N / 2);
+            const int pos = k & (half - 1), grp = k / half;
+            const int i0 = grp * 2 * half + pos, i1 = i0 + half;
+            double2 w = stw[pos * (N / (2 * half))];
+            if (inverse) w.y = -w.y;
+            double2 lo, hi;
+            bfly(buf[i * N + i0], buf[i * N + i1], w, lo, hi);
+            buf[i * N + i0] = lo, buf[i * N + i1] = hi;
+        }
+        __syncthreads();
+    }
+}
+
 // One radix-2 FFT pass of length N along axis `ax` for every line of every
 // pair in the batch.  Tile = B lines (contiguous rows for the last axis,
 // lines adjacent in the last axis otherwise).
@@ -112,49 +160,7 @@ __global__ void __launch_bounds__(kFT) k_fft_pass(FftArgs A)
         buf[i * N + tr] = v;
     }
     __syncthreads();
-    // radix-2 DIT stages, two per barrier: a thread takes the 4 elements
-    // i0 + {0, 1, 2, 3} half of one 4-half block and applies stage `half` and
-    // stage `2 half` to them in registers (the same butterflies and twiddles
-    // as one stage at a time)
-    auto stages = [&](bool inverse) {
-        auto bfly = [](double2 u, double2 x, double2 w, double2 &lo, double2 &hi) {
-            const double2 v = cmul(x, w);
-            lo = make_double2(u.x + v.x, u.y + v.y);
-            hi = make_double2(u.x - v.x, u.y - v.y);
-        };
-        int half = 1;
-        for (; 4 * half <= N; half <<= 2) {
-            for (int b = threadIdx.x; b < B * N / 4; b += kFT) {
-                const int i = b / (N / 4), k = b % (N / 4);
-                const int pos = k % half, grp = k / half;
-                const int i0 = grp * 4 * half + pos;
-                double2 w1 = stw[pos * (N / (2 * half))];
-                double2 wa = stw[pos * (N / (4 * half))], wb = stw[(pos + half) * (N / (4 * half))];
-                if (inverse) w1.y = -w1.y, wa.y = -wa.y, wb.y = -wb.y;
-                double2 *r = buf + i * N + i0;
-                double2 y0, y1, y2, y3, z0, z1, z2, z3;
-                bfly(r[0], r[half], w1, y0, y1);
-                bfly(r[2 * half], r[3 * half], w1, y2, y3);
-                bfly(y0, y2, wa, z0, z2);
-                bfly(y1, y3, wb, z1, z3);
-                r[0] = z0, r[half] = z1, r[2 * half] = z2, r[3 * half] = z3;
-            }
-            __syncthreads();
-        }
-        if (half < N) {  // log2 N odd: the last stage alone
-            for (int b = threadIdx.x; b < B * N / 2; b += kFT) {
-                const int i = b / (N / 2), k = b % (N / 2);
-                const int pos = k & (half - 1), grp = k / half;
-                const int i0 = grp * 2 * half + pos, i1 = i0 + half;
-                double2 w = stw[pos * (N / (2 * half))];
-                if (inverse) w.y = -w.y;
-                double2 lo, hi;
-                bfly(buf[i * N + i0], buf[i * N + i1], w, lo, hi);
-                buf[i * N + i0] = lo, buf[i * N + i1] = hi;
-            }
-            __syncthreads();
-        }
-    };
+    auto stages = [&](bool inverse) { fft_stages<N, B>(buf, stw, inverse); };
     stages(A.inverse != 0);
     if (A.roundtrip) {
         // the same arithmetic as a forward pass storing × λ̂ and an inverse pass
