@@ -378,10 +378,6 @@ dvm_status_t dvm_collide_batched_host(dvm_plan_t P, const double *f_host, double
     // up to the FFT loss's cell pairing, which chunks of even size preserve).
     const int nch = ncells >= 256 ? 4 : 1;
     const int64_t per = nch == 1 ? ncells : (((ncells + nch - 1) / nch) + 1) / 2 * 2;
-    if (!P->cstream[0]) {
-        DVM_CUDA(cudaStreamCreateWithFlags(&P->cstream[0], cudaStreamNonBlocking));
-        DVM_CUDA(cudaStreamCreateWithFlags(&P->cstream[1], cudaStreamNonBlocking));
-    }
     auto copy = [&](double *dst, int64_t dpitch, const double *src, int64_t spitch, int64_t nc, cudaMemcpyKind k,
                     cudaStream_t strm) -> cudaError_t {
         if (dpitch == nodes && spitch == nodes)
@@ -389,6 +385,22 @@ dvm_status_t dvm_collide_batched_host(dvm_plan_t P, const double *f_host, double
         return cudaMemcpy2DAsync(dst, sizeof(double) * dpitch, src, sizeof(double) * spitch, sizeof(double) * nodes,
                                  nc, k, strm);
     };
+    if (nch == 1) {
+        // small batches: copy in, evaluate, copy out, all on the plan's stream
+        // (no copy streams or events: their cross-stream waits cost more than
+        // the overlap they could buy)
+        cudaError_t ce = copy(w.f_stage, nodes, f_host, cell_stride, ncells, cudaMemcpyHostToDevice, P->stream);
+        if (ce != cudaSuccess) return cuda_fail(ce, "host->device copy");
+        if ((st = collide_batched(P, w.f_stage, w.q_stage, ncells, nodes))) return st;
+        ce = copy(Q_host, cell_stride, w.q_stage, nodes, ncells, cudaMemcpyDeviceToHost, P->stream);
+        if (ce == cudaSuccess) ce = cudaStreamSynchronize(P->stream);
+        if (ce != cudaSuccess) return cuda_fail(ce, "device->host copy");
+        return DVM_OK;
+    }
+    if (!P->cstream[0]) {
+        DVM_CUDA(cudaStreamCreateWithFlags(&P->cstream[0], cudaStreamNonBlocking));
+        DVM_CUDA(cudaStreamCreateWithFlags(&P->cstream[1], cudaStreamNonBlocking));
+    }
     std::vector<cudaEvent_t> ev;
     auto fail = [&](dvm_status_t code) {
         for (cudaEvent_t e : ev) cudaEventDestroy(e);
