@@ -150,6 +150,7 @@ struct GainTables {
     double2 *tw = nullptr;    // FFT twiddles exp(-2πik/N), k < N/2
     double *lamhat = nullptr; // [N^d] spectrum of the loss kernel λ (real)
     void *units = nullptr;    // 2D: direction-pair units (dvm_pair2d.cu)
+    std::vector<char> h_units2d;  // host copy of the units (kernel-parameter path of k_tile2d)
     int nunits = 0;
     int maxitems2d = 0;       // 2D: work items of the longest line walk
     double *shat = nullptr;   // spectral path: [A_local][N^d] line-filter spectra (real)

@@ -22,6 +22,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <cstring>
 #include <mutex>
 #include <vector>
 
@@ -330,13 +331,14 @@ __global__ void __launch_bounds__(256) k_small2d_sum_euler(const double *__restr
 constexpr int kTile = 16;             // tile rows
 constexpr int kTileC = TILE2D_COLS;    // tile columns (one warp per row)
 
-__global__ void __launch_bounds__(kTile * kTileC) k_tile2d(const double *__restrict__ f, int64_t f_stride,
-                                                const Unit2D *__restrict__ units, int nunits, int N, int H,
-                                                double *__restrict__ Q, int64_t q_stride)
+// the tile kernel's body; getU(u) returns unit u (shared memory, or the kernel
+// parameter space for up to kParamUnits units: warp-uniform constant-cache loads
+// instead of shared-memory wavefronts)
+template <class GetU>
+__device__ __forceinline__ void tile2d_body(const double *__restrict__ f, int64_t f_stride, int nunits, int N, int H,
+                                            double *__restrict__ Q, int64_t q_stride, double *s2, GetU getU)
 {
-    extern __shared__ __align__(16) double s2[];
     const int PR = kTile + 2 * H, P = kTileC + 2 * H;  // rows, pitch of the tile + halo
-    Unit2D *su = reinterpret_cast<Unit2D *>(s2 + ((PR * P + 1) & ~1));
     const int t = threadIdx.x;
     const int64_t cell = blockIdx.z;
     const int r0 = blockIdx.y * kTile, c0 = blockIdx.x * kTileC;
@@ -346,14 +348,13 @@ __global__ void __launch_bounds__(kTile * kTileC) k_tile2d(const double *__restr
         const int gr = (r0 - H + rr) & (N - 1), gc = (c0 - H + cc) & (N - 1);
         s2[i] = fc[(int64_t)gr * N + gc];
     }
-    for (int i = t; i < nunits; i += blockDim.x) su[i] = units[i];
     __syncthreads();
     const int ty = t / kTileC, tx = t % kTileC;
     const double *c = s2 + (H + ty) * P + (H + tx);
     const double fx = c[0];
     double g = 0.0;
     for (int u = 0; u < nunits; ++u) {
-        const Unit2D U = su[u];
+        const Unit2D U = getU(u);
         const int M = U.M, oa = U.a0 * P + U.a1, ob = U.b0 * P + U.b1;
         double wa0 = fx, wa1 = 0.0, wb0 = fx, wb1 = 0.0, wa2 = 0.0, wa3 = 0.0, wb2 = 0.0, wb3 = 0.0;
         int m = 1;
@@ -381,6 +382,30 @@ __global__ void __launch_bounds__(kTile * kTileC) k_tile2d(const double *__restr
     }
     double *q = Q + cell * q_stride + (int64_t)(r0 + ty) * N + (c0 + tx);
     *q += g;
+}
+
+__global__ void __launch_bounds__(kTile * kTileC) k_tile2d(const double *__restrict__ f, int64_t f_stride,
+                                                const Unit2D *__restrict__ units, int nunits, int N, int H,
+                                                double *__restrict__ Q, int64_t q_stride)
+{
+    extern __shared__ __align__(16) double s2[];
+    const int PR = kTile + 2 * H, P = kTileC + 2 * H;
+    Unit2D *su = reinterpret_cast<Unit2D *>(s2 + ((PR * P + 1) & ~1));
+    for (int i = threadIdx.x; i < nunits; i += blockDim.x) su[i] = units[i];
+    tile2d_body(f, f_stride, nunits, N, H, Q, q_stride, s2, [&](int u) { return su[u]; });
+}
+
+constexpr int kParamUnits = 256;
+struct TileUnits {
+    Unit2D u[kParamUnits];
+};
+
+__global__ void __launch_bounds__(kTile * kTileC) k_tile2d_pu(const double *__restrict__ f, int64_t f_stride,
+                                                   int nunits, int N, int H, double *__restrict__ Q,
+                                                   int64_t q_stride, const __grid_constant__ TileUnits pu)
+{
+    extern __shared__ __align__(16) double s2[];
+    tile2d_body(f, f_stride, nunits, N, H, Q, q_stride, s2, [&](int u) { return pu.u[u]; });
 }
 
 }  // namespace
@@ -530,6 +555,8 @@ dvm_status_t build_pair2d(dvm_plan_s *P)
     for (const Unit2D &U : units)
         maxitems = std::max({maxitems, walk_items(walk_shape(U.a0, P->N), P->N), walk_items(walk_shape(U.b0, P->N), P->N)});
     P->g.maxitems2d = maxitems;
+    P->g.h_units2d.assign(reinterpret_cast<const char *>(units.data()),
+                          reinterpret_cast<const char *>(units.data() + units.size()));
     if (!units.empty()) {
         DVM_CUDA(cudaMalloc(&P->g.units, sizeof(Unit2D) * units.size()));
         DVM_CUDA(cudaMemcpyAsync(P->g.units, units.data(), sizeof(Unit2D) * units.size(), cudaMemcpyHostToDevice,
@@ -585,15 +612,23 @@ dvm_status_t collide_pair2d(dvm_plan_s *P, const double *f, int64_t f_stride, do
             if ((int)set_to.size() <= dev) set_to.resize(dev + 1, 0);
             if (set_to[dev] < tsm) {
                 DVM_CUDA(cudaFuncSetAttribute(k_tile2d, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
+                DVM_CUDA(cudaFuncSetAttribute(k_tile2d_pu, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
                 set_to[dev] = tsm;
             }
         }
         for (int64_t c0 = 0; c0 < ncells; c0 += 65535) {
             const int nc = (int)std::min<int64_t>(65535, ncells - c0);
             LaunchScope ls(P, KC_PAIR2D);
-            k_tile2d<<<dim3(N / kTileC, N / kTile, nc), kTile * kTileC, tsm, P->stream>>>(
-                f + c0 * f_stride, f_stride, reinterpret_cast<const Unit2D *>(P->g.units), nunits, N, P->Ntilde,
-                Q + c0 * q_stride, q_stride);
+            if (nunits <= kParamUnits && (int)P->g.h_units2d.size() == nunits * (int)sizeof(Unit2D)) {
+                TileUnits pu;
+                std::memcpy(pu.u, P->g.h_units2d.data(), sizeof(Unit2D) * (size_t)nunits);
+                k_tile2d_pu<<<dim3(N / kTileC, N / kTile, nc), kTile * kTileC, tsm, P->stream>>>(
+                    f + c0 * f_stride, f_stride, nunits, N, P->Ntilde, Q + c0 * q_stride, q_stride, pu);
+            } else {
+                k_tile2d<<<dim3(N / kTileC, N / kTile, nc), kTile * kTileC, tsm, P->stream>>>(
+                    f + c0 * f_stride, f_stride, reinterpret_cast<const Unit2D *>(P->g.units), nunits, N, P->Ntilde,
+                    Q + c0 * q_stride, q_stride);
+            }
             DVM_CUDA(cudaGetLastError());
         }
         return DVM_OK;
