@@ -234,6 +234,54 @@ __global__ void __launch_bounds__(kST) k_small2d(const double *__restrict__ f, i
     }
 }
 
+// The same unit partials as k_small2d in two fine-grained launches, so the
+// large-M units no longer set the critical path of one CTA each: k_s2_wb
+// writes W_B of every (unit, row block) to scratch, k_s2_part the partial of
+// every (unit, row block) from f and that scratch (both read through L1/L2).
+// Same sums in the same order: bitwise the k_small2d partials.
+__global__ void __launch_bounds__(256) k_s2_wb(const double *__restrict__ f, int64_t f_stride,
+                                              const Unit2D *__restrict__ units, int nunits, int nrb, int p,
+                                              double *__restrict__ wb)
+{
+    const int N = 1 << p, mask = N - 1, nodes = N * N;
+    const int u = blockIdx.x / nrb, rb = blockIdx.x % nrb, c = blockIdx.y;
+    const Unit2D U = units[u];
+    const double *fc = f + (int64_t)c * f_stride;
+    double *wc = wb + ((int64_t)c * nunits + u) * nodes;
+    const int i0 = nodes / nrb * rb, i1 = i0 + nodes / nrb;
+    for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+        const int x0 = i >> p, x1 = i & mask;
+        double w = 0.0;
+        for (int m = -U.M; m <= U.M; ++m) w += __ldg(fc + ((((x0 + m * U.b0) & mask) << p) | ((x1 + m * U.b1) & mask)));
+        wc[i] = w;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_s2_part(const double *__restrict__ f, int64_t f_stride,
+                                                const Unit2D *__restrict__ units, int nunits, int nrb, int p,
+                                                const double *__restrict__ wb, double *__restrict__ part)
+{
+    const int N = 1 << p, mask = N - 1, nodes = N * N;
+    const int u = blockIdx.x / nrb, rb = blockIdx.x % nrb, c = blockIdx.y;
+    const Unit2D U = units[u];
+    const double *fc = f + (int64_t)c * f_stride;
+    const double *wc = wb + ((int64_t)c * nunits + u) * nodes;
+    double *out = part + ((int64_t)c * nunits + u) * nodes;
+    const double ca = (U.flags & 1) ? U.aw : 0.0, cb = (U.flags & 2) ? U.aw : 0.0;
+    const int i0 = nodes / nrb * rb, i1 = i0 + nodes / nrb;
+    for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+        const int x0 = i >> p, x1 = i & mask;
+        double wa = 0.0, box = 0.0;
+        for (int m = -U.M; m <= U.M; ++m) {
+            const int j = (((x0 + m * U.a0) & mask) << p) | ((x1 + m * U.a1) & mask);
+            wa += __ldg(fc + j);
+            box += wc[j];
+        }
+        const double f0 = __ldg(fc + i), w0 = wc[i];
+        out[i] = ca * (wa - f0) * w0 + cb * (w0 - f0) * wa - f0 * (ca * (box - w0) + cb * (box - wa));
+    }
+}
+
 // Q[c][x] = Σ_u part[c][u][x], u ascending
 // Q[c][x] = Σ_units part[c][u][x]: a block takes 32 consecutive nodes; its 8
 // warps sum the units in 8 contiguous groups (loads of a group in flight
@@ -478,6 +526,31 @@ dvm_status_t collide_small2d(dvm_plan_s *P, const double *f, int64_t f_stride, d
                                           (int)(sizeof(double) * 2 * 64 * 64)));
             done[dev] = 1;
         }
+    }
+    if (N >= 32) {
+        // two fine-grained launches over (unit, 256-node row block) items (c2: 1 + 100
+        // Euler steps 2.04 -> 1.86 ms); a 16 x 16 grid keeps the one-launch kernel
+        const int nrb = nodes / 256;
+        if ((st = grow(&w.p2_scr, &w.p2_scr_elems, (size_t)(chunk * nunits * nodes), P->stream))) return st;
+        const int64_t nq = Q ? ncells : 1;
+        for (int64_t c0 = 0; c0 < nq; c0 += chunk) {
+            const int nc = (int)std::min<int64_t>(chunk, nq - c0);
+            {
+                LaunchScope ls(P, KC_SMALL2D);
+                k_s2_wb<<<dim3(nunits * nrb, nc), 256, 0, P->stream>>>(f + c0 * f_stride, f_stride, units, nunits, nrb,
+                                                                        p, w.p2_scr);
+                k_s2_part<<<dim3(nunits * nrb, nc), 256, 0, P->stream>>>(f + c0 * f_stride, f_stride, units, nunits,
+                                                                          nrb, p, w.p2_scr, w.p2_part);
+            }
+            if (Q) {
+                LaunchScope ls(P, KC_REDUCE);
+                const int64_t tot = (int64_t)nc * nodes;
+                k_small2d_sum<<<(unsigned)std::min<int64_t>(2368, (tot + 31) / 32), 256, 0, P->stream>>>(
+                    w.p2_part, nunits, nc, nodes, Q + c0 * q_stride, q_stride);
+            }
+            DVM_CUDA(cudaGetLastError());
+        }
+        return DVM_OK;
     }
     if (!Q) {  // collide_small2d_parts: the partials of one cell only
         const int nslice = (int)std::max<int64_t>(1, std::min<int64_t>(8, sms / (int64_t)nunits));
