@@ -3,6 +3,7 @@
 #include <math.h>
 #include <string.h>
 
+#include <atomic>
 #include <new>
 #include <string>
 #include <vector>
@@ -113,6 +114,14 @@ dvm_status_t check_batch(dvm_plan_s *P, const double *f, double *Q, int64_t ncel
 }
 
 }  // namespace
+
+namespace dvm {
+namespace {
+std::atomic<uint64_t> g_ws_epoch{0};
+}
+uint64_t ws_epoch() { return g_ws_epoch.load(std::memory_order_relaxed); }
+void ws_epoch_bump() { g_ws_epoch.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace dvm
 
 extern "C" {
 
@@ -302,12 +311,99 @@ dvm_status_t dvm_set_stream(dvm_plan_t P, void *stream)
     return DVM_OK;
 }
 
+namespace {
+void drop_collide_graph(dvm_plan_s *P)
+{
+    if (P->cg.exec) cudaGraphExecDestroy(P->cg.exec);
+    P->cg = dvm_plan_s::CollideGraph{};
+}
+
+// Capture collide_batched(f, Q) on the plan's graph stream; true with cg.exec set
+// if the whole call was capturable (any synchronising or allocating call inside
+// fails the capture: the caller then runs it directly).
+bool capture_collide(dvm_plan_s *P, const double *f, double *Q, int64_t ncells, int64_t cell_stride)
+{
+    if (!P->gstream) {
+        if (cudaStreamCreateWithFlags(&P->gstream, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&P->gev[0], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&P->gev[1], cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+    }
+    cudaStream_t user = P->stream;
+    const uint64_t l0 = P->launches, e0 = ws_epoch();
+    P->stream = P->gstream;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaError_t ce = cudaStreamBeginCapture(P->gstream, cudaStreamCaptureModeThreadLocal);
+    dvm_status_t st = DVM_OK;
+    if (ce == cudaSuccess) {
+        st = collide_batched(P, f, Q, ncells, cell_stride);
+        ce = cudaStreamEndCapture(P->gstream, &graph);
+        if (st == DVM_OK && ce == cudaSuccess && ws_epoch() == e0) ce = cudaGraphInstantiate(&exec, graph, 0);
+    }
+    P->stream = user;
+    if (graph) cudaGraphDestroy(graph);
+    const bool ok = st == DVM_OK && ce == cudaSuccess && exec && ws_epoch() == e0;
+    if (!ok) {
+        if (exec) cudaGraphExecDestroy(exec);
+        cudaGetLastError();
+        P->launches = l0;
+        return false;
+    }
+    P->cg.exec = exec;
+    P->cg.launches = P->launches - l0;
+    P->launches = l0;
+    return true;
+}
+}  // namespace
+
 dvm_status_t dvm_collide_batched(dvm_plan_t P, const double *f, double *Q, int64_t ncells, int64_t cell_stride)
 {
     NvtxRange nvtx_range("dvm_collide_batched");
     dvm_status_t st = check_batch(P, f, Q, ncells, &cell_stride);
     if (st) return st;
-    return collide_batched(P, f, Q, ncells, cell_stride);
+    // small batches are host-launch bound: the second identical call is captured
+    // as one CUDA graph, later identical calls replay it (same kernels, same bits)
+    const bool small = ncells > 0 && (uint64_t)ncells * (uint64_t)nodes_of(P) <= (1ull << 22);
+    if (!P->use_graphs || P->profiling || !small) return collide_batched(P, f, Q, ncells, cell_stride);
+    auto &g = P->cg;
+    const bool same = g.f == f && g.Q == Q && g.n == ncells && g.stride == cell_stride && g.version == P->version &&
+                      g.epoch == ws_epoch();
+    if (same && g.state == 1) {
+        const cudaError_t ce = cudaGraphLaunch(g.exec, P->stream);
+        if (ce == cudaSuccess) {
+            P->launches += g.launches;
+            return DVM_OK;
+        }
+        cudaGetLastError();
+        drop_collide_graph(P);
+        return collide_batched(P, f, Q, ncells, cell_stride);
+    }
+    if (same && g.state == 0) {
+        if (capture_collide(P, f, Q, ncells, cell_stride)) {
+            g.state = 1;
+            const cudaError_t ce = cudaGraphLaunch(g.exec, P->stream);
+            if (ce == cudaSuccess) {
+                P->launches += g.launches;
+                return DVM_OK;
+            }
+            cudaGetLastError();
+            drop_collide_graph(P);
+            return collide_batched(P, f, Q, ncells, cell_stride);
+        }
+        g.state = 2;
+        return collide_batched(P, f, Q, ncells, cell_stride);
+    }
+    if (!same) {
+        drop_collide_graph(P);
+        st = collide_batched(P, f, Q, ncells, cell_stride);
+        g.f = f, g.Q = Q, g.n = ncells, g.stride = cell_stride;
+        g.version = P->version, g.epoch = ws_epoch(), g.state = 0;
+        return st;
+    }
+    return collide_batched(P, f, Q, ncells, cell_stride);  // capture failed for this key
 }
 
 dvm_status_t dvm_collide_batched_levels(const dvm_plan_t *plans, int nlevels, const double *f, double *Q,
@@ -617,6 +713,7 @@ dvm_status_t dvm_set_graphs(dvm_plan_t P, int enable)
         set_error("NULL argument");
         return DVM_E_NULL;
     }
+    ++P->version;  // invalidates a captured collide graph
     P->use_graphs = enable != 0;
     return DVM_OK;
 }
@@ -665,6 +762,7 @@ dvm_status_t dvm_set_path(dvm_plan_t P, int path)
         set_error("NULL argument");
         return DVM_E_NULL;
     }
+    ++P->version;  // invalidates a captured collide graph
     if (path < 0 || path > 7) {
         set_error("path must be 0 (auto), 1 (v1 orbit sweeps), 2 (gain3d / pair2d line walks), 3 (spectral "
                   "reference), 4 (3D FFT gain), 5 (2D small grids), 6 (3D N = 32 spectral direction pairs) or 7 "
@@ -681,6 +779,7 @@ dvm_status_t dvm_set_tuning(dvm_plan_t P, const char *key, int value)
         set_error("NULL argument");
         return DVM_E_NULL;
     }
+    ++P->version;  // invalidates a captured collide graph
     const std::string k(key);
     auto bad = [&]() {
         set_error("dvm_set_tuning: bad value for " + k);
@@ -716,6 +815,7 @@ dvm_status_t dvm_set_weights(dvm_plan_t P, const double *a_box, const double *b_
         set_error("NULL argument");
         return DVM_E_NULL;
     }
+    ++P->version;  // invalidates a captured collide graph
     return set_weights(P, a_box, b_box);
 }
 
@@ -737,6 +837,7 @@ dvm_status_t dvm_plan_destroy(dvm_plan_t P)
         return DVM_E_NULL;
     }
     cudaStreamSynchronize(P->stream);
+    if (P->cg.exec) cudaGraphExecDestroy(P->cg.exec);
     if (P->gstream) {
         cudaStreamSynchronize(P->gstream);
         cudaStreamDestroy(P->gstream);

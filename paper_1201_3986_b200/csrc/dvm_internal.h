@@ -219,6 +219,19 @@ struct dvm_plan_s {
     cudaStream_t cstream[2] = {nullptr, nullptr};  // host variant: host->device / device->host copy streams
     cudaEvent_t gev[2] = {nullptr, nullptr};
     std::vector<dvm::ProfRec> prof;
+    // Repeated dvm_collide_batched calls with the same arguments on small batches
+    // replay one captured CUDA graph (captured at the second identical call):
+    // `version` changes with every plan setting, dvm::ws_epoch() with every
+    // workspace reallocation; either invalidates the graph.
+    uint64_t version = 0;
+    struct CollideGraph {
+        cudaGraphExec_t exec = nullptr;
+        const double *f = nullptr;
+        double *Q = nullptr;
+        int64_t n = -1, stride = 0;
+        uint64_t version = 0, epoch = 0, launches = 0;
+        int state = 0;  // 0 first call seen, 1 graph ready, 2 capture failed (no retry for this key)
+    } cg;
 };
 
 namespace dvm {
@@ -262,10 +275,15 @@ dvm_status_t cuda_fail(cudaError_t err, const char *what);
     } while (0)
 
 // Grow-only device workspace buffer (stream-synchronised before a reallocation).
+// process-wide workspace epoch: bumped by every workspace reallocation (any plan)
+uint64_t ws_epoch();
+void ws_epoch_bump();
+
 template <typename T>
 dvm_status_t grow(T **ptr, size_t *cap, size_t need, cudaStream_t s)
 {
     if (*cap >= need) return DVM_OK;
+    ws_epoch_bump();
     cudaError_t e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
     if (*ptr) cudaFree(*ptr);
