@@ -145,7 +145,13 @@ DVM_API dvm_status_t dvm_collide(dvm_plan_t plan, const double *f, double *Q);
  * dvm_collide plus DVM_E_SHAPE (ncells < 0, cell_stride < N^d, overflow).
  * The plan grows a device workspace on first use of a batch size (3D: ~3 × 16 B
  * per node per cell pair plus a 256 MiB FFT batch; 2D: <= 512 MiB of per-pair
- * partials); DVM_E_NOMEM if it cannot. */
+ * partials); DVM_E_NOMEM if it cannot.  Small batches (ncells N^d <= 2^22)
+ * are host-launch bound: the second call with the same (f, Q, ncells,
+ * cell_stride) is captured as one CUDA graph on a plan-owned stream and every
+ * later identical call replays it on the plan's stream (the same kernels, so
+ * the same bits; f is read at replay time).  Any dvm_set_* call on the plan and
+ * any workspace reallocation invalidate the graph; dvm_set_graphs(plan, 0)
+ * turns capture off. */
 DVM_API dvm_status_t dvm_collide_batched(dvm_plan_t plan, const double *f, double *Q, int64_t ncells,
                                  int64_t cell_stride);
 
@@ -203,7 +209,8 @@ DVM_API dvm_status_t dvm_euler(dvm_plan_t plan, double *f, double dt, int nsteps
  * plan's stream); results are identical to direct launches. */
 DVM_API dvm_status_t dvm_rk2(dvm_plan_t plan, double *f, double dt, int nsteps, double *moments_host);
 
-/* Enable (default) or disable the CUDA-graph replay of the time steppers. */
+/* Enable (default) or disable the CUDA-graph replay of the time steppers and of
+ * repeated small dvm_collide_batched calls. */
 DVM_API dvm_status_t dvm_set_graphs(dvm_plan_t plan, int enable);
 
 /* Per-kernel timing with CUDA events recorded on the plan's stream around

@@ -283,6 +283,47 @@ def test_constant_field(d, N, Nbar):
     assert np.abs(Qc).max() <= 1e-13 * G.max()
 
 
+@pytest.mark.parametrize("name", ["c1", "c3", "c4"])
+def test_collide_graph_replay(name):
+    """Repeated dvm_collide_batched calls with the same buffers replay one captured
+    CUDA graph (include/dvm.h): the same bits as direct launches, f read at
+    replay time, and plan settings / workspace growth invalidate the graph."""
+    cfg = dvm_inputs.CONFIGS[name]
+    f0 = dvm_inputs.make(name)
+    p = _plan(cfg.d, cfg.N, cfg.Nbar)
+    ref = _plan(cfg.d, cfg.N, cfg.Nbar)
+    ref.set_graphs(False)
+    f = torch.from_numpy(f0.copy()).cuda()
+    q = torch.empty_like(f)
+    want = _gpu(ref, f0)
+    l0 = p.launches()
+    for _ in range(4):  # direct, captured, replayed, replayed
+        p.collide(f, q)
+        torch.cuda.synchronize()
+        assert np.array_equal(q.cpu().numpy(), want)
+    assert p.launches() - l0 >= 4  # replays still count their kernels
+    # new data in the same buffer: the replay reads it
+    f1 = f0 * (1.0 + 0.05 * np.cos(np.arange(f0.size)).reshape(f0.shape))
+    f.copy_(torch.from_numpy(f1))
+    p.collide(f, q)
+    torch.cuda.synchronize()
+    assert np.array_equal(q.cpu().numpy(), _gpu(ref, f1))
+    # a larger batch grows the workspace; the old key is captured afresh afterwards
+    f2 = torch.from_numpy(np.concatenate([f1, f0], axis=0)).cuda()
+    p.collide(f2)
+    for _ in range(3):
+        p.collide(f, q)
+        torch.cuda.synchronize()
+        assert np.array_equal(q.cpu().numpy(), _gpu(ref, f1))
+    # a setting change invalidates the graph (path 1 = v1 sweeps: equal to rounding)
+    p.set_path(1)
+    ref.set_path(1)
+    for _ in range(3):
+        p.collide(f, q)
+        torch.cuda.synchronize()
+    assert np.array_equal(q.cpu().numpy(), _gpu(ref, f1))
+
+
 def test_determinism_bitwise():
     cfg = dvm_inputs.CONFIGS["c4"]
     f = dvm_inputs.make("c4")
