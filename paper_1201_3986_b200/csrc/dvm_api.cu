@@ -123,6 +123,88 @@ uint64_t ws_epoch() { return g_ws_epoch.load(std::memory_order_relaxed); }
 void ws_epoch_bump() { g_ws_epoch.fetch_add(1, std::memory_order_relaxed); }
 }  // namespace dvm
 
+namespace {
+void drop_collide_graph(dvm_plan_s *P)
+{
+    if (P->cg.exec) cudaGraphExecDestroy(P->cg.exec);
+    P->cg = dvm_plan_s::CollideGraph{};
+}
+
+// Capture work() (which issues everything on P->stream) on the plan's graph
+// stream; true with cg.exec set if the whole call was capturable (any
+// synchronising or allocating call inside fails the capture: the caller then
+// runs it directly).
+template <class Work>
+bool capture_work(dvm_plan_s *P, Work &&work)
+{
+    if (!P->gstream) {
+        if (cudaStreamCreateWithFlags(&P->gstream, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&P->gev[0], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&P->gev[1], cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+    }
+    cudaStream_t user = P->stream;
+    const uint64_t l0 = P->launches, e0 = ws_epoch();
+    P->stream = P->gstream;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaError_t ce = cudaStreamBeginCapture(P->gstream, cudaStreamCaptureModeThreadLocal);
+    dvm_status_t st = DVM_OK;
+    if (ce == cudaSuccess) {
+        st = work();
+        ce = cudaStreamEndCapture(P->gstream, &graph);
+        if (st == DVM_OK && ce == cudaSuccess && ws_epoch() == e0) ce = cudaGraphInstantiate(&exec, graph, 0);
+    }
+    P->stream = user;
+    if (graph) cudaGraphDestroy(graph);
+    const bool ok = st == DVM_OK && ce == cudaSuccess && exec && ws_epoch() == e0;
+    if (!ok) {
+        if (exec) cudaGraphExecDestroy(exec);
+        cudaGetLastError();
+        P->launches = l0;
+        return false;
+    }
+    P->cg.exec = exec;
+    P->cg.launches = P->launches - l0;
+    P->launches = l0;
+    return true;
+}
+
+// work() through the graph cache, keyed by (kind, a, b, n, stride) with the plan
+// version and the workspace epoch: small batches are host-launch bound, so the
+// second identical call is captured as one CUDA graph and later identical calls
+// replay it (same kernels and copies, same bits)
+template <class Work>
+dvm_status_t run_cached(dvm_plan_s *P, int kind, const void *a, const void *b, int64_t ncells, int64_t cell_stride,
+                        Work &&work)
+{
+    const bool small = ncells > 0 && (uint64_t)ncells * (uint64_t)nodes_of(P) <= (1ull << 22);
+    if (!P->use_graphs || P->profiling || !small) return work();
+    auto &g = P->cg;
+    const bool same = g.kind == kind && g.f == a && g.Q == b && g.n == ncells && g.stride == cell_stride &&
+                      g.version == P->version && g.epoch == ws_epoch();
+    if (same && g.state == 0) g.state = capture_work(P, work) ? 1 : 2;
+    if (same && g.state == 1) {
+        const cudaError_t ce = cudaGraphLaunch(g.exec, P->stream);
+        if (ce == cudaSuccess) {
+            P->launches += g.launches;
+            return DVM_OK;
+        }
+        cudaGetLastError();
+        drop_collide_graph(P);
+        return work();
+    }
+    if (same) return work();  // capture failed for this key
+    drop_collide_graph(P);
+    const dvm_status_t st = work();
+    g.kind = kind, g.f = a, g.Q = b, g.n = ncells, g.stride = cell_stride;
+    g.version = P->version, g.epoch = ws_epoch(), g.state = 0;
+    return st;
+}
+}  // namespace
+
 extern "C" {
 
 int dvm_abi_version(void) { return DVM_ABI_VERSION; }
@@ -311,99 +393,13 @@ dvm_status_t dvm_set_stream(dvm_plan_t P, void *stream)
     return DVM_OK;
 }
 
-namespace {
-void drop_collide_graph(dvm_plan_s *P)
-{
-    if (P->cg.exec) cudaGraphExecDestroy(P->cg.exec);
-    P->cg = dvm_plan_s::CollideGraph{};
-}
-
-// Capture collide_batched(f, Q) on the plan's graph stream; true with cg.exec set
-// if the whole call was capturable (any synchronising or allocating call inside
-// fails the capture: the caller then runs it directly).
-bool capture_collide(dvm_plan_s *P, const double *f, double *Q, int64_t ncells, int64_t cell_stride)
-{
-    if (!P->gstream) {
-        if (cudaStreamCreateWithFlags(&P->gstream, cudaStreamNonBlocking) != cudaSuccess ||
-            cudaEventCreateWithFlags(&P->gev[0], cudaEventDisableTiming) != cudaSuccess ||
-            cudaEventCreateWithFlags(&P->gev[1], cudaEventDisableTiming) != cudaSuccess) {
-            cudaGetLastError();
-            return false;
-        }
-    }
-    cudaStream_t user = P->stream;
-    const uint64_t l0 = P->launches, e0 = ws_epoch();
-    P->stream = P->gstream;
-    cudaGraph_t graph = nullptr;
-    cudaGraphExec_t exec = nullptr;
-    cudaError_t ce = cudaStreamBeginCapture(P->gstream, cudaStreamCaptureModeThreadLocal);
-    dvm_status_t st = DVM_OK;
-    if (ce == cudaSuccess) {
-        st = collide_batched(P, f, Q, ncells, cell_stride);
-        ce = cudaStreamEndCapture(P->gstream, &graph);
-        if (st == DVM_OK && ce == cudaSuccess && ws_epoch() == e0) ce = cudaGraphInstantiate(&exec, graph, 0);
-    }
-    P->stream = user;
-    if (graph) cudaGraphDestroy(graph);
-    const bool ok = st == DVM_OK && ce == cudaSuccess && exec && ws_epoch() == e0;
-    if (!ok) {
-        if (exec) cudaGraphExecDestroy(exec);
-        cudaGetLastError();
-        P->launches = l0;
-        return false;
-    }
-    P->cg.exec = exec;
-    P->cg.launches = P->launches - l0;
-    P->launches = l0;
-    return true;
-}
-}  // namespace
-
 dvm_status_t dvm_collide_batched(dvm_plan_t P, const double *f, double *Q, int64_t ncells, int64_t cell_stride)
 {
     NvtxRange nvtx_range("dvm_collide_batched");
     dvm_status_t st = check_batch(P, f, Q, ncells, &cell_stride);
     if (st) return st;
-    // small batches are host-launch bound: the second identical call is captured
-    // as one CUDA graph, later identical calls replay it (same kernels, same bits)
-    const bool small = ncells > 0 && (uint64_t)ncells * (uint64_t)nodes_of(P) <= (1ull << 22);
-    if (!P->use_graphs || P->profiling || !small) return collide_batched(P, f, Q, ncells, cell_stride);
-    auto &g = P->cg;
-    const bool same = g.f == f && g.Q == Q && g.n == ncells && g.stride == cell_stride && g.version == P->version &&
-                      g.epoch == ws_epoch();
-    if (same && g.state == 1) {
-        const cudaError_t ce = cudaGraphLaunch(g.exec, P->stream);
-        if (ce == cudaSuccess) {
-            P->launches += g.launches;
-            return DVM_OK;
-        }
-        cudaGetLastError();
-        drop_collide_graph(P);
-        return collide_batched(P, f, Q, ncells, cell_stride);
-    }
-    if (same && g.state == 0) {
-        if (capture_collide(P, f, Q, ncells, cell_stride)) {
-            g.state = 1;
-            const cudaError_t ce = cudaGraphLaunch(g.exec, P->stream);
-            if (ce == cudaSuccess) {
-                P->launches += g.launches;
-                return DVM_OK;
-            }
-            cudaGetLastError();
-            drop_collide_graph(P);
-            return collide_batched(P, f, Q, ncells, cell_stride);
-        }
-        g.state = 2;
-        return collide_batched(P, f, Q, ncells, cell_stride);
-    }
-    if (!same) {
-        drop_collide_graph(P);
-        st = collide_batched(P, f, Q, ncells, cell_stride);
-        g.f = f, g.Q = Q, g.n = ncells, g.stride = cell_stride;
-        g.version = P->version, g.epoch = ws_epoch(), g.state = 0;
-        return st;
-    }
-    return collide_batched(P, f, Q, ncells, cell_stride);  // capture failed for this key
+    return run_cached(P, 0, f, Q, ncells, cell_stride,
+                      [&]() { return collide_batched(P, f, Q, ncells, cell_stride); });
 }
 
 dvm_status_t dvm_collide_batched_levels(const dvm_plan_t *plans, int nlevels, const double *f, double *Q,
@@ -485,12 +481,15 @@ dvm_status_t dvm_collide_batched_host(dvm_plan_t P, const double *f_host, double
         // small batches: copy in, evaluate, copy out, all on the plan's stream
         // (no copy streams or events: their cross-stream waits cost more than
         // the overlap they could buy)
-        cudaError_t ce = copy(w.f_stage, nodes, f_host, cell_stride, ncells, cudaMemcpyHostToDevice, P->stream);
-        if (ce != cudaSuccess) return cuda_fail(ce, "host->device copy");
-        if ((st = collide_batched(P, w.f_stage, w.q_stage, ncells, nodes))) return st;
-        ce = copy(Q_host, cell_stride, w.q_stage, nodes, ncells, cudaMemcpyDeviceToHost, P->stream);
-        if (ce == cudaSuccess) ce = cudaStreamSynchronize(P->stream);
-        if (ce != cudaSuccess) return cuda_fail(ce, "device->host copy");
+        cudaError_t ce0 = copy(w.f_stage, nodes, f_host, cell_stride, ncells, cudaMemcpyHostToDevice, P->stream);
+        if (ce0 != cudaSuccess) return cuda_fail(ce0, "host->device copy");
+        st = run_cached(P, 0, w.f_stage, w.q_stage, ncells, nodes,
+                        [&]() { return collide_batched(P, w.f_stage, w.q_stage, ncells, nodes); });
+        if (st) return st;
+        ce0 = copy(Q_host, cell_stride, w.q_stage, nodes, ncells, cudaMemcpyDeviceToHost, P->stream);
+        if (ce0 != cudaSuccess) return cuda_fail(ce0, "device->host copy");
+        const cudaError_t ce = cudaStreamSynchronize(P->stream);
+        if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamSynchronize");
         return DVM_OK;
     }
     if (!P->cstream[0]) {

@@ -226,10 +226,10 @@ struct dvm_plan_s {
     uint64_t version = 0;
     struct CollideGraph {
         cudaGraphExec_t exec = nullptr;
-        const double *f = nullptr;
-        double *Q = nullptr;
+        const void *f = nullptr, *Q = nullptr;
         int64_t n = -1, stride = 0;
         uint64_t version = 0, epoch = 0, launches = 0;
+        int kind = -1;  // 0 device buffers, 1 host buffers (copies captured too)
         int state = 0;  // 0 first call seen, 1 graph ready, 2 capture failed (no retry for this key)
     } cg;
 };
