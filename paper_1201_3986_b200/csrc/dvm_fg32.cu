@@ -173,6 +173,24 @@ __global__ void __launch_bounds__(128) k_f32_plane(const double2 *__restrict__ f
     for (int i = t; i < K32 * K32; i += 128) dst[i] = buf[(i >> 5) * P32 + (i & 31)];
 }
 
+// Q := −f Λ for row y from the loss array's plane transform (the loss of eq:decD
+// as one convolution, reading R21): the inverse DFT along ξ_0 gives N^3 Λ.
+__device__ __forceinline__ void f32_xloss_row(const double *__restrict__ f, const double2 *__restrict__ Zl,
+                                              double *__restrict__ Q, int y, double2 *buf, const double2 *tw32)
+{
+    const int t = threadIdx.x;
+    const double2 *src = Zl + y * K32;
+    for (int i = t; i < K32 * K32; i += 128) buf[(i >> 5) * P32 + (i & 31)] = src[(i >> 5) * K32 * K32 + (i & 31)];
+    __syncthreads();
+    ifft32_lines(buf, 1, P32, tw32);
+    constexpr double inv = 1.0 / (double)K32N;
+    for (int i = t; i < K32 * K32; i += 128) {
+        const int x = i >> 5, z = i & 31;
+        const int n = (x * K32 + y) * K32 + z;
+        Q[n] = -f[n] * (buf[x * P32 + z].x * inv);
+    }
+}
+
 // One CTA per (row y, pair chunk): for every pair of the chunk, the inverse DFT
 // along ξ_0 of Z[p][:][y][:] gives T_a + i T_b on the 32 x 32 nodes (x, y, z);
 // then G += a_a S_a T_a + a_b S_b T_b (S as taps of f), G in registers, written
@@ -181,7 +199,8 @@ __global__ void __launch_bounds__(128) k_f32_xgain(const double *__restrict__ f,
                                                    const uint32_t *__restrict__ off, int mmax2,
                                                    const int4 *__restrict__ ru, const double *__restrict__ aw,
                                                    int nloc, int npairs, int ppc, uint32_t H,
-                                                   double *__restrict__ part)
+                                                   double *__restrict__ part, const double2 *__restrict__ Zl,
+                                                   double *__restrict__ Q)
 {
     __shared__ double2 buf[K32 * P32];
     __shared__ double2 tw32[K32];
@@ -191,6 +210,11 @@ __global__ void __launch_bounds__(128) k_f32_xgain(const double *__restrict__ f,
         double s, c;
         sincospi(2.0 * t / K32, &s, &c);
         tw32[t] = make_double2(c, s);
+    }
+    if (chunk == (int)gridDim.y - 1) {  // the last row of blocks: Q := −f Λ (concurrent with the gain chunks)
+        __syncthreads();
+        f32_xloss_row(f, Zl, Q, y, buf, tw32);
+        return;
     }
     double G[8];
 #pragma unroll
@@ -243,22 +267,14 @@ __global__ void __launch_bounds__(128) k_f32_xloss(const double *__restrict__ f,
 {
     __shared__ double2 buf[K32 * P32];
     __shared__ double2 tw32[K32];
-    const int y = blockIdx.x, t = threadIdx.x;
+    const int t = threadIdx.x;
     if (t < K32) {
         double s, c;
         sincospi(2.0 * t / K32, &s, &c);
         tw32[t] = make_double2(c, s);
     }
-    const double2 *src = Zl + y * K32;
-    for (int i = t; i < K32 * K32; i += 128) buf[(i >> 5) * P32 + (i & 31)] = src[(i >> 5) * K32 * K32 + (i & 31)];
     __syncthreads();
-    ifft32_lines(buf, 1, P32, tw32);
-    constexpr double inv = 1.0 / (double)K32N;
-    for (int i = t; i < K32 * K32; i += 128) {
-        const int x = i >> 5, z = i & 31;
-        const int n = (x * K32 + y) * K32 + z;
-        Q[n] = -f[n] * (buf[x * P32 + z].x * inv);
-    }
+    f32_xloss_row(f, Zl, Q, blockIdx.x, buf, tw32);
 }
 
 // Q[x] += Σ_chunk part[chunk][x], chunks in order (Q holds −fΛ)
@@ -362,17 +378,18 @@ dvm_status_t collide_fg32(dvm_plan_s *P, const double *f, int64_t f_stride, doub
                                                                    nloc, npairs, g.lamhat, w.f32_z);
             DVM_CUDA(cudaGetLastError());
         }
-        {
+        if (nloc == 0) {
             LaunchScope ls(P, KC_FG32);
             k_f32_xloss<<<K32, 128, 0, P->stream>>>(f + c * f_stride, w.f32_z + (size_t)npairs * K32N, Q + c * q_stride);
             DVM_CUDA(cudaGetLastError());
+            continue;
         }
-        if (nloc == 0) continue;
         {
+            // the gain chunks and, in one more row of blocks, the loss Q := −fΛ
             LaunchScope ls(P, KC_FG32);
-            k_f32_xgain<<<dim3(K32, nchunks), 128, 0, P->stream>>>(f + c * f_stride, w.f32_z, g.f32_off,
-                                                                  2 * g.f32_mmax, g.f32_rec, g.f32_aw, nloc, npairs,
-                                                                  ppc, P->pk.H, w.f32_part);
+            k_f32_xgain<<<dim3(K32, nchunks + 1), 128, 0, P->stream>>>(
+                f + c * f_stride, w.f32_z, g.f32_off, 2 * g.f32_mmax, g.f32_rec, g.f32_aw, nloc, npairs, ppc, P->pk.H,
+                w.f32_part, w.f32_z + (size_t)npairs * K32N, Q + c * q_stride);
             DVM_CUDA(cudaGetLastError());
         }
         {
