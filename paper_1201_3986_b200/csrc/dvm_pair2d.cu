@@ -663,12 +663,6 @@ dvm_status_t collide_pair2d(dvm_plan_s *P, const double *f, int64_t f_stride, do
     if (st) return st;
     const int nunits = P->g.nunits;
     if (nunits == 0) return DVM_OK;
-    // cell chunks bounded by the scratch + partial budget
-    const size_t per_cell = sizeof(double) * 2 * (size_t)nunits * nodes;
-    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(ncells, (int64_t)((512ull << 20) / per_cell)));
-    Workspace &w = P->ws;
-    if ((st = grow(&w.p2_scr, &w.p2_scr_elems, (size_t)(chunk * nunits * nodes), P->stream))) return st;
-    if ((st = grow(&w.p2_part, &w.p2_part_elems, (size_t)(chunk * nunits * nodes), P->stream))) return st;
     // the tile kernel when its tile + halo fits shared memory and the batch has enough
     // tiles for most SMs (c3: 128 tiles; dvm_set_path 7 forces it, 2 the line walks)
     const size_t tsm = tile2d_smem(P->Ntilde, nunits);
@@ -706,6 +700,12 @@ dvm_status_t collide_pair2d(dvm_plan_s *P, const double *f, int64_t f_stride, do
         }
         return DVM_OK;
     }
+    // the line-walk kernels: cell chunks bounded by the scratch + partial budget
+    const size_t per_cell = sizeof(double) * 2 * (size_t)nunits * nodes;
+    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(ncells, (int64_t)((512ull << 20) / per_cell)));
+    Workspace &w = P->ws;
+    if ((st = grow(&w.p2_scr, &w.p2_scr_elems, (size_t)(chunk * nunits * nodes), P->stream))) return st;
+    if ((st = grow(&w.p2_part, &w.p2_part_elems, (size_t)(chunk * nunits * nodes), P->stream))) return st;
     const int items = P->g.maxitems2d;  // largest walk of any unit (shorter walks exit early)
     for (int64_t c0 = 0; c0 < ncells; c0 += chunk) {
         const int nc = (int)std::min<int64_t>(chunk, ncells - c0);
