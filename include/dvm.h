@@ -149,7 +149,9 @@ DVM_API dvm_status_t dvm_collide(dvm_plan_t plan, const double *f, double *Q);
  * are host-launch bound: the second call with the same (f, Q, ncells,
  * cell_stride) is captured as one CUDA graph on a plan-owned stream and every
  * later identical call replays it on the plan's stream (the same kernels, so
- * the same bits; f is read at replay time).  Any dvm_set_* call on the plan and
+ * the same bits; f is read at replay time; not for the persistent 3D N = 64
+ * and batched N = 32 kernels, whose CTA groups need a cooperative launch).
+ * Any dvm_set_* call on the plan and
  * any workspace reallocation invalidate the graph; dvm_set_graphs(plan, 0)
  * turns capture off. */
 DVM_API dvm_status_t dvm_collide_batched(dvm_plan_t plan, const double *f, double *Q, int64_t ncells,

@@ -181,7 +181,10 @@ dvm_status_t run_cached(dvm_plan_s *P, int kind, const void *a, const void *b, i
                         Work &&work)
 {
     const bool small = ncells > 0 && (uint64_t)ncells * (uint64_t)nodes_of(P) <= (1ull << 22);
-    if (!P->use_graphs || P->profiling || !small) return work();
+    // the persistent 3D gain kernels (N = 64; N = 32 beyond 2 cells or forced) rely
+    // on a cooperative launch for co-residency of their CTA groups: never captured
+    const bool coop = P->d == 3 && (P->N == 64 || (P->N == 32 && (ncells > 2 || (P->path_mode != 0 && P->path_mode != 6))));
+    if (!P->use_graphs || P->profiling || !small || coop) return work();
     auto &g = P->cg;
     const bool same = g.kind == kind && g.f == a && g.Q == b && g.n == ncells && g.stride == cell_stride &&
                       g.version == P->version && g.epoch == ws_epoch();
