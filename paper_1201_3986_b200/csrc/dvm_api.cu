@@ -185,6 +185,12 @@ dvm_status_t run_cached(dvm_plan_s *P, int kind, const void *a, const void *b, i
     // on a cooperative launch for co-residency of their CTA groups: never captured
     const bool coop = P->d == 3 && (P->N == 64 || (P->N == 32 && (ncells > 2 || (P->path_mode != 0 && P->path_mode != 6))));
     if (!P->use_graphs || P->profiling || !small || coop) return work();
+    // a caller capturing its own graph on the plan's stream gets the plain launches
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(P->stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+        cudaGetLastError();
+        return work();
+    }
     auto &g = P->cg;
     const bool same = g.kind == kind && g.f == a && g.Q == b && g.n == ncells && g.stride == cell_stride &&
                       g.version == P->version && g.epoch == ws_epoch();

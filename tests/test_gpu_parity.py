@@ -324,6 +324,31 @@ def test_collide_graph_replay(name):
     assert np.array_equal(q.cpu().numpy(), _gpu(ref, f1))
 
 
+def test_collide_inside_user_graph_capture():
+    """A caller capturing the plan's stream into its own CUDA graph gets plain
+    launches (the collide graph cache steps aside): replaying the caller's graph
+    gives the direct result."""
+    cfg = dvm_inputs.CONFIGS["c1"]
+    f0 = dvm_inputs.make("c1")
+    p = _plan(cfg.d, cfg.N, cfg.Nbar)
+    f = torch.from_numpy(f0.copy()).cuda()
+    q = torch.empty_like(f)
+    want = _gpu(p, f0)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        p.collide(f, q)  # warm on this stream (workspace, tables)
+        p.collide(f, q)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        p.collide(f, q)
+        p.collide(f, q)
+    q.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(q.cpu().numpy(), want)
+
+
 def test_determinism_bitwise():
     cfg = dvm_inputs.CONFIGS["c4"]
     f = dvm_inputs.make("c4")
