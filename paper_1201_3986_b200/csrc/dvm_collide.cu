@@ -601,8 +601,9 @@ dvm_status_t collide_levels(dvm_plan_s *const *plans, int nlevels, const double 
         const int64_t n = cnt[lv];
         if (n == 0) continue;
         if (n == ncells) return collide_batched(plans[lv], f, Q, ncells, stride);  // one level: no gather
-        if ((st = grow(&w.lv_f, &w.lv_f_elems, (size_t)n * g.nodes, P0->stream))) return st;
-        if ((st = grow(&w.lv_q, &w.lv_q_elems, (size_t)n * g.nodes, P0->stream))) return st;
+        // gather buffers for the whole batch once (bucket sizes change from call to call)
+        if ((st = grow(&w.lv_f, &w.lv_f_elems, (size_t)ncells * g.nodes, P0->stream))) return st;
+        if ((st = grow(&w.lv_q, &w.lv_q_elems, (size_t)ncells * g.nodes, P0->stream))) return st;
         const int64_t *ix = w.lv_idx + off;
         {
             LaunchScope ls(P0, KC_ZERO);

@@ -286,6 +286,9 @@ dvm_status_t grow(T **ptr, size_t *cap, size_t need, cudaStream_t s)
     ws_epoch_bump();
     cudaError_t e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+    // a regrowth takes at least 1.5x the old capacity (batches that creep up, e.g.
+    // the level buckets of space-dependent N̄, reallocate O(log) times)
+    if (*cap > 0 && need < *cap + *cap / 2) need = *cap + *cap / 2;
     if (*ptr) cudaFree(*ptr);
     *ptr = nullptr;
     *cap = 0;
