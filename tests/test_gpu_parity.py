@@ -665,6 +665,48 @@ def test_adaptive_reference_policy():
     assert lv.shape == (2,) and np.all(delta < 0.05) and np.all(lv == 2)
 
 
+def test_adaptive_levels_with_transport():
+    """Space-dependent N̄ inside a transport + collision splitting (PAPER.md:
+    907-911; tools/inhomogeneous.py at a small size): levels re-chosen every step,
+    bucket sizes changing from step to step; mass conserved to rounding, every
+    step's Q per cell equal to that cell's single-level evaluation, and the
+    adaptive trajectory close to the uniform-N̄ one."""
+    from paper_1201_3986_b200.adaptive import AdaptiveNbar, equilibrium_levels
+    N, X, levels = 32, 16, [2, 7]
+    h, dx = 16.0 / N, 1.0 / X
+    v = (torch.arange(N, dtype=torch.float64) - N // 2) * h
+    VX, VY = torch.meshgrid(v, v, indexing="ij")
+    dt = 0.5 * dx / float(v.abs().max())
+    def mx(rho, ux, T):
+        return (rho / (2 * np.pi * T) * torch.exp(-((VX - ux) ** 2 + VY ** 2) / (2 * T))).reshape(-1)
+    f0 = torch.stack([0.5 * (mx(1.0, 1.2, 0.5) + mx(1.0, -1.2, 0.5)) if 0.3 < (i + 0.5) * dx < 0.7
+                      else mx(1.0 + 0.3 * np.sin(2 * np.pi * (i + 0.5) * dx), 0.0, 1.0) for i in range(X)]).cuda()
+    vx = VX.reshape(-1).cuda()
+    pos = (vx > 0).double()
+    def transport(f):
+        return f - dt / dx * vx * (pos * (f - torch.roll(f, 1, 0)) + (1 - pos) * (torch.roll(f, -1, 0) - f))
+    ad = AdaptiveNbar(2, N, levels)
+    single = {nb: _plan(2, N, nb, Ntilde=ad.Ntilde) for nb in levels}
+    full = single[levels[-1]]
+    fa, fu = f0.clone(), f0.clone()
+    m0 = float(fa.sum())
+    seen = set()
+    for _ in range(6):
+        fa, fu = transport(fa), transport(fu)
+        nb, _ = equilibrium_levels(fa, 2, N, 8.0, levels, [0.02])
+        seen.add(int((nb == levels[0]).sum()))
+        qa = ad.collide(fa, nb)
+        qs = torch.stack([single[int(nb[c])].collide(fa[c].contiguous()) for c in range(X)])
+        torch.cuda.synchronize()
+        np.testing.assert_allclose(qa.cpu().numpy(), qs.cpu().numpy(), rtol=0,
+                                   atol=1e-13 * float(qs.abs().max()))
+        fa += dt * qa
+        fu += dt * full.collide(fu)
+    assert abs(float(fa.sum()) - m0) <= 1e-12 * m0
+    assert 0 < min(seen) < X  # both levels in use
+    assert float((fa - fu).abs().sum() / fu.abs().sum()) < 1e-3
+
+
 # ---------------------------------------------------------------- spectral reference path (dvm_set_path(3))
 @pytest.mark.parametrize("d,N,Nbar,Nt,cells", [(2, 16, 4, 4, 1), (2, 64, 8, 14, 2), (3, 32, 2, 5, 1), (3, 32, 4, 7, 2)])
 def test_spectral_path_matches_oracle(d, N, Nbar, Nt, cells):
