@@ -64,6 +64,16 @@ struct FgArgs {
                           // 4 skip the taps
 };
 
+// tap loads of phase B, not allocated in L1 (no reuse there: hit rate 1.8 %)
+__device__ __forceinline__ double2 ld2_tap(const double2 *a, uint64_t pol)
+{
+    double2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                 : "=d"(v.x), "=d"(v.y)
+                 : "l"(a), "l"(pol));
+    return v;
+}
+
 __device__ __forceinline__ double2 cmul(double2 a, double2 b)
 {
     return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
@@ -123,7 +133,7 @@ __device__ __forceinline__ void group_wait(const unsigned int *ctrs, unsigned in
 // Phase A of k_fg2: 16 points per thread, 64 = 4 × 16 in both in-plane passes
 // (radix-4 over the high index in registers, one warp-private 16 × 16
 // transpose, a 16-point DFT; one CTA-wide exchange between the two axes), so
-// a plane costs 3 role barriers.  Plane ξ_x = g, thread t = (yl, zl), zl = t & 15,
+// a plane costs 2 role barriers plus one mbarrier only the storing warp waits on.  Plane ξ_x = g, thread t = (yl, zl), zl = t & 15,
 // yl = t >> 4, holds f̂(g, ξ_y = yl + 16 b, ξ_z = zl + 16 a), a, b < 4:
 //   z: radix-4 over a, × ω^{zl kp1}; y: radix-4 over b, × ω^{yl kq1}    (ω = e^{2πi/64})
 //   warp-private transpose: thread (yl, c = kp1 + 4 kq1) gets the 16 zl
@@ -137,6 +147,7 @@ __device__ __forceinline__ void group_wait(const unsigned int *ctrs, unsigned in
 // 512 contiguous bytes.
 // ============================================================================
 constexpr int kRegA2 = FG2_REGA, kRegB2 = 256 - FG2_REGA;
+constexpr int kStoreWarp = 0;  // phase-A warp issuing the ring bulk stores (warp 7 measured 1.5 % slower)
 constexpr int F2Q = FN2 / 4 + 4;  // CTA-exchange pitch of one kq1 quarter [16 yl][64 z] (+4: conflict-free writes)
 
 struct Fg2Smem {
@@ -227,6 +238,7 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
     __shared__ uint32_t s_tmem;
     __shared__ __align__(8) uint64_t s_mbar;  // FG_BULK: completion of the phase-A bulk loads
     __shared__ __align__(8) uint64_t s_xbar[2], s_rbar[2];  // phase-B exchange buffer written / read
+    __shared__ __align__(8) uint64_t s_obar;  // phase A: the plane's output rows are in the exchange buffer
 
     const bool roleA = threadIdx.x < kRoleT;
     const int t = threadIdx.x & (kRoleT - 1);
@@ -254,6 +266,7 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
     }
     if (threadIdx.x == 0) {
         mbar_init(&s_mbar, 1);
+        mbar_init(&s_obar, kRoleT);
         for (int k = 0; k < 2; ++k) {
             mbar_init(&s_xbar[k], kRoleT);
             mbar_init(&s_rbar[k], kRoleT);
@@ -275,6 +288,7 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
         }
     };
     uint32_t mph = 0;
+    uint32_t oph = 0;
 
     if (roleA) {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegA2));
@@ -351,7 +365,7 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
                     for (int n = 0; n < 16; ++n)
                         v[n] = x1w[(c_me >> 2) * 16 * FN + 16 * (c_me & 3) + (n ^ sw)];
                     idft16(v);  // z = kp1 + 4 kp2: v[kp2], kp1 = c_me & 3
-                    if (warp == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // ex is read
+                    if (warp == kStoreWarp) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // ex is read
                     role_sync(bar);  // [2] staging and the exchange buffer are free
                     if (!lastp)
                         issue(fh, g + CL, -1);
@@ -377,9 +391,11 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
 #pragma unroll
                         for (int k = 0; k < 16; ++k) own[k * FN] = v[k];
                     }
-                    role_sync(bar);  // [4]
-                    if (warp == 0) {
-                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    // [4] as an mbarrier only the storing warp waits on
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    mbar_arrive(&s_obar);
+                    if (warp == kStoreWarp) {
+                        mbar_wait(&s_obar, oph);
 #pragma unroll
                         for (int h = 0; h < 2; ++h) {
                             const int idx = lane + 32 * h, q = idx >> 4, r = idx & 15;
@@ -392,8 +408,9 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
                         }
                         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                     }
+                    oph ^= 1;
                 }
-                if (warp == 0) {
+                if (warp == kStoreWarp) {
                     // the step's planes are in global memory before the release below
                     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
                     asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -500,13 +517,13 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
                             const uint32_t b2 = swar_add(n[0], so[k0 + 2], H2), b3 = swar_add(n[0], so[k0 + 3], H2);
 #pragma unroll
                             for (int q = 0; q < 4; ++q) {
-                                a[q] = ld2_nc_hint(fc + ((b0 + (uint32_t)q * 8u * FN2) & (uint32_t)(FNODES - 1)), keep);
-                                c[q] = ld2_nc_hint(fc + ((b1 + (uint32_t)q * 8u * FN2) & (uint32_t)(FNODES - 1)), keep);
+                                a[q] = ld2_tap(fc + ((b0 + (uint32_t)q * 8u * FN2) & (uint32_t)(FNODES - 1)), keep);
+                                c[q] = ld2_tap(fc + ((b1 + (uint32_t)q * 8u * FN2) & (uint32_t)(FNODES - 1)), keep);
                             }
 #pragma unroll
                             for (int q = 0; q < 4; ++q) {
-                                a2[q] = ld2_nc_hint(fc + ((b2 + (uint32_t)q * 8u * FN2) & (uint32_t)(FNODES - 1)), keep);
-                                c2[q] = ld2_nc_hint(fc + ((b3 + (uint32_t)q * 8u * FN2) & (uint32_t)(FNODES - 1)), keep);
+                                a2[q] = ld2_tap(fc + ((b2 + (uint32_t)q * 8u * FN2) & (uint32_t)(FNODES - 1)), keep);
+                                c2[q] = ld2_tap(fc + ((b3 + (uint32_t)q * 8u * FN2) & (uint32_t)(FNODES - 1)), keep);
                             }
 #pragma unroll
                             for (int q = 0; q < 4; ++q) S[q] = add2(S[q], add2(a[q], c[q]));
@@ -522,8 +539,8 @@ __global__ void __launch_bounds__(2 * kRoleT, 1) k_fg2(FgArgs A)
                             const uint32_t b0 = swar_add(n[0], o0, H2), b1 = swar_add(n[0], o1, H2);
 #pragma unroll
                             for (int q = 0; q < 4; ++q) {
-                                a[q] = ld2_nc_hint(fc + ((b0 + (uint32_t)q * 8u * FN2) & (uint32_t)(FNODES - 1)), keep);
-                                c[q] = ld2_nc_hint(fc + ((b1 + (uint32_t)q * 8u * FN2) & (uint32_t)(FNODES - 1)), keep);
+                                a[q] = ld2_tap(fc + ((b0 + (uint32_t)q * 8u * FN2) & (uint32_t)(FNODES - 1)), keep);
+                                c[q] = ld2_tap(fc + ((b1 + (uint32_t)q * 8u * FN2) & (uint32_t)(FNODES - 1)), keep);
                             }
 #pragma unroll
                             for (int q = 0; q < 4; ++q) S[q] = add2(S[q], add2(a[q], c[q]));
