@@ -230,14 +230,15 @@ def _kernel_metrics(name: str):
 
 # what limits the dominant kernel (ncu evidence in profiles/r02/SUMMARY.md)
 BINDING = {
-    "k_fg2": "latency-bound: phase-B tap and ring loads waiting on L2 (long scoreboard), SM L1/shared pipe ~60%, "
-             "fp64 pipe ~24%, issue ~29%; see profiles/r02/SUMMARY.md",
+    "k_fg2": "SM L1/shared data pipe (~70%, shared by both warp roles: four register re-arrangements of every "
+             "point per step plus misaligned tap loads) and latency (16 warps per SM); fp64 pipe ~29%, issue ~37%; "
+             "see DESIGN.md 6 (data-movement floor) and profiles/r02/SUMMARY.md",
     "k_gain3d": "SM L1/shared-memory pipe (sliding-program loads + scattered frame gather/store); "
                 "see profiles/r01/SUMMARY.md",
 }
 
 
-def _roofline(prof, psteps, bytes_per_eval, evals_per_step, cells=None):
+def _roofline(prof, psteps, bytes_per_eval, evals_per_step, cells=None, workload=None):
     """roofline object for the dominant kernel: algorithmic (streaming-
     formulation) bytes of the evaluations one launch covers / its CUDA-event
     launch time, against the measured HBM copy bandwidth."""
@@ -277,6 +278,15 @@ def _roofline(prof, psteps, bytes_per_eval, evals_per_step, cells=None):
         r["fp64_pipe_pct"] = km.get("fp64_pipe_pct")
         r["l1tex_pct"] = km.get("l1tex_pct")
         r["ncu_source"] = km.get("source")
+    elif workload is not None and _kernel_metrics("workload:" + workload):
+        # c1-c4: the ncu totals of one whole evaluation (every kernel of it) against
+        # this run's per-evaluation device time (libdvm's per-launch events)
+        wm = _kernel_metrics("workload:" + workload)
+        step_s = total / psteps / 1e3
+        r["dram_GBps"] = wm["dram_bytes_per_eval"] * evals_per_step / step_s / 1e9
+        r["fp64_pipe_pct"] = round(wm["fp64_pipe_pct"], 2)
+        r["l1tex_pct"] = round(wm["l1tex_pct"], 2)
+        r["ncu_source"] = wm.get("source")
     return r
 
 
@@ -475,7 +485,7 @@ def run_grid(args):
             step()
     prof = plan.profile_read()
     plan.profile(False)
-    roofline = _roofline(prof, psteps, (A + 2) * 8.0 * nodes, 1, cells=1)
+    roofline = _roofline(prof, psteps, (A + 2) * 8.0 * nodes, 1, cells=1, workload=name)
     # e2e with host buffers through the C ABI: f in, Q (and for c2 the final f) out
     fh = torch.from_numpy(f0.copy()).pin_memory()
     qh = torch.empty_like(fh).pin_memory()

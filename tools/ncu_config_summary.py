@@ -1,11 +1,20 @@
 """Summarise tools/ncu_configs.sh CSVs: per kernel, launches, mean duration,
-DRAM bytes per launch, fp64-pipe and l1tex utilisation (duration-weighted)."""
+DRAM bytes per launch, fp64-pipe and l1tex utilisation (duration-weighted).
+With --write, also store the whole evaluation's totals (the CSV holds exactly
+one evaluation) as profiles/kernel_metrics.json["workload:<cfg>"], which
+bench.py attaches to the c1-c4 lines (DRAM GB/s and fp64 pipe
+per config).  Usage: python tools/ncu_config_summary.py [--write] gpurun_out/ncu_c*.csv"""
 import collections
 import csv
+import json
+import os
 import re
 import sys
 
-for path in sys.argv[1:]:
+write = "--write" in sys.argv
+paths = [a for a in sys.argv[1:] if a != "--write"]
+store = {}
+for path in paths:
     rows = list(csv.reader(open(path)))
     start = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
     hdr = rows[start]
@@ -38,3 +47,22 @@ for path in sys.argv[1:]:
     for k, a in agg.items():
         n, t = a[0], a[1]
         print(f"{k:24s} {n:8d} {t / n:9.2f} {a[2] / n / 1e6:15.3f} {a[3] / max(t, 1e-9):6.1f} {a[4] / max(t, 1e-9):7.1f}")
+    T = sum(a[1] for a in agg.values())
+    tot = {"eval_kernel_us": T, "launches": sum(a[0] for a in agg.values()),
+           "dram_bytes_per_eval": sum(a[2] for a in agg.values()),
+           "fp64_pipe_pct": sum(a[3] for a in agg.values()) / max(T, 1e-9),
+           "l1tex_pct": sum(a[4] for a in agg.values()) / max(T, 1e-9)}
+    print(f"{'evaluation':24s} {tot['launches']:8d} {T:9.2f} {tot['dram_bytes_per_eval'] / 1e6:15.3f} "
+          f"{tot['fp64_pipe_pct']:6.1f} {tot['l1tex_pct']:7.1f}")
+    m = re.search(r"ncu_(c[1-5])", path)
+    if m:
+        tot["source"] = (f"ncu --metrics (gpu__time_duration, dram__bytes_read/write, sm__pipe_fp64_cycles_active, "
+                         f"l1tex__throughput) of every kernel of one {m.group(1)} evaluation after warm-up "
+                         f"(tools/ncu_configs.sh), duration-weighted; profiles/r02/config_kernels_ncu.txt")
+        store["workload:" + m.group(1)] = tot
+if write and store:
+    kp = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "kernel_metrics.json")
+    km = json.load(open(kp)) if os.path.exists(kp) else {}
+    km.update(store)
+    json.dump(km, open(kp, "w"), indent=1)
+    print("wrote", ", ".join(store), "to", kp)
