@@ -497,6 +497,30 @@ def test_fgain3d_path_matches_frame_path(Nbar, Nt, cells):
     _assert_parity(q4[cells - 1][pts], Qo[0], f"fgain3d N̄={Nbar} Ñ={Nt}")
 
 
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_parity_c5_strong_scaling_rank_blocks(world):
+    """c5 as one rank of bench.py's strong-scaling run launches it (BASELINE c5:
+    512 cells sharded across 2/4/8 GPUs; parallel.cell_range gives the last rank
+    512/world contiguous cells, one batched call, so another direction-chunk
+    count than the 512-cell launch).  Six cells of the block (first, last and
+    four seeded) on 128 nodes each (as in the 512-cell test) against the oracle."""
+    from paper_1201_3986_b200.parallel import cell_range
+    cfg = dvm_inputs.CONFIGS["c5"]
+    first, count = cell_range(512, world - 1, world)
+    f = dvm_inputs.make("c5")[first:first + count]
+    p = _plan(3, cfg.N, cfg.Nbar)
+    Qg = _gpu(p, f)
+    rng = np.random.default_rng(world)
+    cells = sorted({0, count - 1, *(int(c) for c in rng.choice(count, size=4, replace=False))})
+    pts = np.stack([_c5_points(f[c], 300 + c) for c in cells])
+    Qo, _, _ = oracle.collide(f[cells], 3, cfg.N, cfg.Nbar, p.Ntilde, cfg.L, points=pts, diagnostics=False)
+    worst = max(_assert_parity(Qg[c][pts[i]], Qo[i], f"c5 world {world} block cell {first + c}")
+                for i, c in enumerate(cells))
+    print(f"c5 rank {world - 1}/{world} ({count} cells): worst {worst:.3e}")
+    sums = Qg.sum(axis=1)
+    assert np.all(np.abs(sums) <= 1e-12 * np.abs(Qg).sum(axis=1))
+
+
 def test_fgain3d_chunked_rounds_match_frame_path():
     """A batch with more pairs than groups and several direction chunks per pair
     (20 cells = 10 pairs on 9 groups: the chunk rule picks more than one chunk
