@@ -415,7 +415,7 @@ def run_grid(args):
 
     import dvm_inputs
     from paper_1201_3986_b200 import Plan
-    from paper_1201_3986_b200.parallel import DirectionSharded
+    from paper_1201_3986_b200.parallel import DirectionSharded, PeerDirectionSharded
 
     name = args.workload
     cfg = dvm_inputs.CONFIGS[name]
@@ -439,7 +439,10 @@ def run_grid(args):
             plan.euler(fw, 0.01, 100)
         evals = 101
     else:
-        ev = DirectionSharded(cfg.d, cfg.N, cfg.Nbar)
+        # --reduce peer: the partials are pushed into every rank's peer window over
+        # NVLink and added in rank order (dvm_collide_push / dvm_peer_reduce)
+        ev = (PeerDirectionSharded(cfg.d, cfg.N, cfg.Nbar, ncells=1) if args.reduce == "peer"
+              else DirectionSharded(cfg.d, cfg.N, cfg.Nbar))
         plan = ev.plan
 
         def step():
@@ -525,7 +528,8 @@ def run_grid(args):
         e2e_ms = float(t.item())
     if rank == 0:
         cpu = cpu_baseline(name, 8.0) if (world == 1 and not args.no_cpu_baseline) else None
-        par = ("replicas" if c2 else "direction-sharded (2D: pair units) + NCCL all-reduce") + f" x{world}"
+        red = "one-shot peer-memory reduction" if args.reduce == "peer" else "NCCL all-reduce"
+        par = ("replicas" if c2 else f"direction-sharded (2D: pair units) + {red}") + f" x{world}"
         line = {"metric": f"Q(f,f) evals/sec, {name}", "value": value, "unit": UNIT, "n_gpus": world,
                 "steps": reps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
                 "scaling": "weak" if c2 else "strong", "vs_baseline": None, "dtype": "f64",
@@ -631,6 +635,8 @@ def main():
                     help="c5: global cells (strong) or cells per rank (weak)")
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--reduce", default="nccl", choices=["nccl", "peer"],
+                    help="c1/c3/c4 direction shards: NCCL all-reduce or the peer-window push + reduce")
     ap.add_argument("--workload", default="c5", choices=["c1", "c2", "c3", "c4", "c5"],
                     help="c5 (default, the BASELINE metric) or one of the single-grid configs")
     ap.add_argument("--dry-run", action="store_true",

@@ -187,6 +187,53 @@ DVM_API dvm_status_t dvm_collide_batched_levels(const dvm_plan_t *plans, int nle
 DVM_API dvm_status_t dvm_collide_batched_host(dvm_plan_t plan, const double *f_host, double *Q_host,
                                       int64_t ncells, int64_t cell_stride);
 
+/* ---- Direction-shard reduction over peer memory (one GPU per rank) ----------
+ * Q is a sum over the directions (eq:decD; "completely
+ * parallelizable"): rank r of a direction-sharded set of
+ * plans (dvm_plan_ex shard_rank = r, shard_world = W) evaluates the partial
+ * Q_r of its LPT share, and Q = Σ_r Q_r.  Instead of a separate all-reduce,
+ * the evaluation pushes Q_r straight into every rank's PEER WINDOW over
+ * NVLink (P2P stores), and each rank then adds the W slots of its own window
+ * in rank order (one-shot reduction, identical bits on every rank).
+ *
+ * A peer window (one per rank, same ncells everywhere) is a device buffer of
+ * dvm_peer_window_bytes(plan, ncells, W) bytes: W slots of ncells × N^d
+ * doubles (slot r holds rank r's partial) followed by W uint32 arrival
+ * counters.  dvm_peer_window_alloc allocates it (cudaMalloc on the plan's
+ * device, counters zeroed; free with dvm_peer_window_free).  Other ranks map
+ * it through CUDA IPC: dvm_ipc_handle writes the 64-byte handle of a device
+ * allocation, dvm_ipc_open maps a peer's handle into this process (peer access
+ * enabled lazily), dvm_ipc_close unmaps it.
+ *
+ * dvm_collide_push(plan, f, ncells, windows, rank, world, epoch)
+ *   f:       DEVICE, ncells cells of N^d doubles (contiguous), the same f on
+ *            every rank.
+ *   windows: HOST array of `world` DEVICE pointers, windows[r] = rank r's
+ *            window as mapped in this process (windows[rank] = the local one).
+ *   rank, world: must equal the plan's shard_rank / shard_world.
+ *   epoch:   1 for the first push into these windows, +1 per later call.
+ *   Evaluates Q_rank into slot `rank` of the local window, copies it into slot
+ *   `rank` of every other window, then (after a system-scope fence) adds the
+ *   arrival of every push CTA to counter `rank` of every window.  Never waits
+ *   for other ranks; stream-ordered on the plan's stream.
+ * dvm_peer_reduce(plan, window, Q, ncells, world, epoch)
+ *   Waits on the device until every counter of the LOCAL window shows the
+ *   pushes of `epoch`, then Q = Σ_{r=0}^{world-1} slot r (in r order).  Every
+ *   rank must have called dvm_collide_push for this epoch (on its own GPU),
+ *   or this call never completes.
+ * Errors: DVM_E_NULL, DVM_E_SHAPE (ncells, world), DVM_E_STATE (rank/world
+ * differ from the plan's shard, epoch 0), DVM_E_NOMEM, DVM_E_CUDA. */
+DVM_API size_t dvm_peer_window_bytes(dvm_plan_t plan, int64_t ncells, int world);
+DVM_API dvm_status_t dvm_peer_window_alloc(dvm_plan_t plan, int64_t ncells, int world, void **out);
+DVM_API dvm_status_t dvm_peer_window_free(void *window);
+DVM_API dvm_status_t dvm_ipc_handle(const void *dptr, unsigned char handle[64]);
+DVM_API dvm_status_t dvm_ipc_open(const unsigned char handle[64], void **out);
+DVM_API dvm_status_t dvm_ipc_close(void *dptr);
+DVM_API dvm_status_t dvm_collide_push(dvm_plan_t plan, const double *f, int64_t ncells, void *const *windows,
+                                      int rank, int world, unsigned int epoch);
+DVM_API dvm_status_t dvm_peer_reduce(dvm_plan_t plan, const void *window, double *Q, int64_t ncells, int world,
+                                     unsigned int epoch);
+
 /* Moments of one cell (device f): out_host[0] = h^d sum f, out_host[1..d] =
  * h^d sum v f, out_host[d+1] = h^d sum |v|^2 f (reading R16).  Synchronous,
  * deterministic. */

@@ -85,6 +85,14 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "dvm_set_weights": ([P, V, V], ctypes.c_int),
         "dvm_set_tuning": ([P, ctypes.c_char_p, ctypes.c_int], ctypes.c_int),
         "dvm_collide_batched_levels": ([V, ctypes.c_int, V, V, I64, I64, V], ctypes.c_int),
+        "dvm_peer_window_bytes": ([P, I64, ctypes.c_int], ctypes.c_size_t),
+        "dvm_peer_window_alloc": ([P, I64, ctypes.c_int, ctypes.POINTER(V)], ctypes.c_int),
+        "dvm_peer_window_free": ([V], ctypes.c_int),
+        "dvm_ipc_handle": ([V, ctypes.c_char_p], ctypes.c_int),
+        "dvm_ipc_open": ([ctypes.c_char_p, ctypes.POINTER(V)], ctypes.c_int),
+        "dvm_ipc_close": ([V], ctypes.c_int),
+        "dvm_collide_push": ([P, V, I64, V, ctypes.c_int, ctypes.c_int, ctypes.c_uint], ctypes.c_int),
+        "dvm_peer_reduce": ([P, V, V, I64, ctypes.c_int, ctypes.c_uint], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -186,6 +194,31 @@ class Plan:
         return out
 
     collide_batched = collide
+
+    # ------------------------------------------------ peer-memory shard reduction
+    def peer_window_alloc(self, ncells: int, world: int) -> int:
+        """This rank's peer window (include/dvm.h): device pointer as an int."""
+        out = ctypes.c_void_p()
+        _check(load().dvm_peer_window_alloc(self._h, ncells, world, ctypes.byref(out)), "dvm_peer_window_alloc")
+        return int(out.value)
+
+    def peer_window_bytes(self, ncells: int, world: int) -> int:
+        return int(load().dvm_peer_window_bytes(self._h, ncells, world))
+
+    def collide_push(self, f, windows, rank: int, world: int, epoch: int):
+        """Q_rank of this shard into slot `rank` of every window (windows: device
+        pointers as mapped in this process, windows[rank] the local one)."""
+        lib, _, n = self._prep(f, f)
+        arr = (ctypes.c_void_p * len(windows))(*[ctypes.c_void_p(int(w)) for w in windows])
+        _check(lib.dvm_collide_push(self._h, _dptr(f), n, ctypes.cast(arr, ctypes.c_void_p), rank, world, epoch),
+               "dvm_collide_push")
+
+    def peer_reduce(self, window: int, out, world: int, epoch: int):
+        """out = sum of the window's slots in rank order, once every push of `epoch` arrived."""
+        lib, out, n = self._prep(out, out)
+        _check(lib.dvm_peer_reduce(self._h, ctypes.c_void_p(int(window)), _dptr(out), n, world, epoch),
+               "dvm_peer_reduce")
+        return out
 
     def collide_host(self, f_host: np.ndarray, out: Optional[np.ndarray] = None) -> np.ndarray:
         """End-to-end through the C ABI with HOST buffers (copies inside the call)."""
@@ -318,3 +351,27 @@ class Plan:
 
     def __exit__(self, *exc):
         self.close()
+
+
+def peer_window_free(window: int):
+    _check(load().dvm_peer_window_free(ctypes.c_void_p(int(window))), "dvm_peer_window_free")
+
+
+def ipc_handle(dptr: int) -> bytes:
+    """64-byte CUDA IPC handle of a device allocation (e.g. a peer window)."""
+    buf = ctypes.create_string_buffer(64)
+    _check(load().dvm_ipc_handle(ctypes.c_void_p(int(dptr)), buf), "dvm_ipc_handle")
+    return buf.raw
+
+
+def ipc_open(handle: bytes) -> int:
+    """Map another process's allocation; returns the device pointer here."""
+    if len(handle) != 64:
+        raise ValueError("CUDA IPC handles are 64 bytes")
+    out = ctypes.c_void_p()
+    _check(load().dvm_ipc_open(ctypes.c_char_p(bytes(handle)), ctypes.byref(out)), "dvm_ipc_open")
+    return int(out.value)
+
+
+def ipc_close(dptr: int):
+    _check(load().dvm_ipc_close(ctypes.c_void_p(int(dptr))), "dvm_ipc_close")

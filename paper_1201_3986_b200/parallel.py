@@ -99,3 +99,54 @@ class DirectionSharded:
 
     def __call__(self, f, out=None):
         return sharded_collide(lambda x: self.plan.collide(x, out), f, self.group)
+
+
+def exchange_handles(handle: bytes, group=None) -> list:
+    """Every rank's 64-byte IPC handle, in rank order (all_gather_object; the
+    handles are host bytes, so this runs on gloo and NCCL groups alike)."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    out = [None] * world
+    dist.all_gather_object(out, handle, group=group)
+    return out
+
+
+class PeerDirectionSharded:
+    """Direction-sharded evaluation of a batch whose reduction runs over peer
+    memory instead of NCCL (include/dvm.h, dvm_collide_push / dvm_peer_reduce):
+    this rank's partial Q_r is pushed into slot r of every rank's peer window
+    over NVLink, then every rank adds its window's slots in rank order.  The
+    windows are exchanged once, at construction, as CUDA IPC handles."""
+
+    def __init__(self, d: int, N: int, Nbar: int, ncells: int = 1, group=None, **plan_kw):
+        import torch.distributed as dist
+        from . import dvm
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.ncells = ncells
+        self.plan = dvm.Plan(d, N, Nbar, shard_rank=self.rank, shard_world=self.world, **plan_kw)
+        self.window = self.plan.peer_window_alloc(ncells, self.world)
+        handles = exchange_handles(dvm.ipc_handle(self.window), group) if self.world > 1 else [None]
+        self.windows = [self.window if r == self.rank else dvm.ipc_open(h) for r, h in enumerate(handles)]
+        self.epoch = 0
+        if self.world > 1:
+            dist.barrier(group)  # every window is mapped before anyone pushes
+
+    def __call__(self, f, out=None):
+        import torch
+        if f.numel() != self.ncells * self.plan.nodes:
+            raise ValueError("f must hold the ncells given at construction")
+        if out is None:
+            out = torch.empty_like(f)
+        self.epoch += 1
+        self.plan.collide_push(f, self.windows, self.rank, self.world, self.epoch)
+        return self.plan.peer_reduce(self.window, out, self.world, self.epoch)
+
+    def close(self):
+        from . import dvm
+        for r, w in enumerate(self.windows):
+            if r != self.rank and w:
+                dvm.ipc_close(w)
+        if self.window:
+            dvm.peer_window_free(self.window)
+        self.windows, self.window = [], 0

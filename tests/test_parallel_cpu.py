@@ -138,3 +138,32 @@ def test_cell_range():
                 pos += c
     with pytest.raises(ValueError):
         parallel.cell_range(4, 2, 2)
+
+
+def _handle_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        hs = parallel.exchange_handles(bytes([rank + 1]) * 64)
+        q.put((rank, hs))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_window_handle_exchange_gloo():
+    """The host side of the peer-memory reduction (parallel.PeerDirectionSharded):
+    every rank receives every rank's 64-byte IPC handle, in rank order."""
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_handle_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = [bytes([r + 1]) * 64 for r in range(world)]
+    assert all(got[r] == want for r in range(world))
