@@ -215,7 +215,9 @@ DVM_API dvm_status_t dvm_collide_batched_host(dvm_plan_t plan, const double *f_h
  *   Evaluates Q_rank into slot `rank` of the local window, copies it into slot
  *   `rank` of every other window, then (after a system-scope fence) adds the
  *   arrival of every push CTA to counter `rank` of every window.  Never waits
- *   for other ranks; stream-ordered on the plan's stream.
+ *   for other ranks; stream-ordered on the plan's stream.  A repeated call with
+ *   the same f and windows on a small batch replays the evaluation and the
+ *   push as one CUDA graph (as dvm_collide_batched does).
  * dvm_peer_reduce(plan, window, Q, ncells, world, epoch)
  *   Waits on the device until every counter of the LOCAL window shows the
  *   pushes of `epoch`, then Q = Σ_{r=0}^{world-1} slot r (in r order).  Every

@@ -224,12 +224,13 @@ struct dvm_plan_s {
     // `version` changes with every plan setting, dvm::ws_epoch() with every
     // workspace reallocation; either invalidates the graph.
     uint64_t version = 0;
+    uint64_t peer_key = 0;  // hash of the last dvm_collide_push window set (a new set bumps `version`)
     struct CollideGraph {
         cudaGraphExec_t exec = nullptr;
         const void *f = nullptr, *Q = nullptr;
         int64_t n = -1, stride = 0;
         uint64_t version = 0, epoch = 0, launches = 0;
-        int kind = -1;  // 0 device buffers, 1 host buffers (copies captured too)
+        int kind = -1;  // 0 device buffers, 1 host buffers (copies captured too), 2 peer push
         int state = 0;  // 0 first call seen, 1 graph ready, 2 capture failed (no retry for this key)
     } cg;
 };
@@ -312,6 +313,12 @@ dvm_status_t moments(dvm_plan_s *P, const double *f, double *dev_out_row);
 dvm_status_t axpy(dvm_plan_s *P, double *f, const double *q, double dt);
 dvm_status_t moments_ctr(dvm_plan_s *P, const double *f, double *dev_base, int *dev_ctr);
 dvm_status_t rk2_stage(dvm_plan_s *P, int stage, double *f, double *f1, const double *q, double dt);
+// peer-memory shard reduction (dvm_peer.cu): argument checks of dvm_collide_push
+// (sets *mine = slot `rank` of the local window) and the push launch
+dvm_status_t peer_push_check(dvm_plan_s *P, const double *f, int64_t ncells, void *const *windows, int rank,
+                             int world, unsigned int epoch, double **mine);
+dvm_status_t peer_push_launch(dvm_plan_s *P, const double *mine, int64_t n, void *const *windows, int rank,
+                              int world);
 dvm_status_t collide_levels(dvm_plan_s *const *plans, int nlevels, const double *f, double *Q, int64_t ncells,
                             int64_t stride, const int *level);
 dvm_status_t copy_cells(dvm_plan_s *P, const double *src, const int64_t *si, double *dst, const int64_t *di,

@@ -116,6 +116,46 @@ dvm_status_t check_peer(dvm_plan_s *P, int64_t ncells, int world)
 }
 
 }  // namespace
+
+dvm_status_t peer_push_check(dvm_plan_s *P, const double *f, int64_t ncells, void *const *windows, int rank,
+                             int world, unsigned int epoch, double **mine)
+{
+    if (!P || !f || !windows) {
+        set_error("NULL argument");
+        return DVM_E_NULL;
+    }
+    dvm_status_t st = check_peer(P, ncells, world);
+    if (st) return st;
+    if (rank != P->shard_rank || epoch == 0) {
+        set_error(epoch == 0 ? "epoch must be >= 1" : "rank must equal the plan's shard_rank");
+        return DVM_E_STATE;
+    }
+    for (int r = 0; r < world; ++r)
+        if (!windows[r]) {
+            set_error("NULL peer window");
+            return DVM_E_NULL;
+        }
+    *mine = (double *)windows[rank] + (size_t)rank * (size_t)(ncells * nodes_per_cell(P));
+    return DVM_OK;
+}
+
+dvm_status_t peer_push_launch(dvm_plan_s *P, const double *mine, int64_t n, void *const *windows, int rank,
+                              int world)
+{
+    const size_t cofs = slots_bytes(n, world);
+    PeerPtrs pp;
+    for (int r = 0; r < world; ++r) {
+        pp.slot[r] = (double2 *)((double *)windows[r] + (size_t)rank * n);
+        pp.ctr[r] = (unsigned int *)((char *)windows[r] + cofs) + rank;
+    }
+    {
+        LaunchScope ls(P, KC_REDUCE);
+        k_peer_push<<<push_blocks(n), kPeerThreads, 0, P->stream>>>((const double2 *)mine, n / 2, pp, world, rank);
+    }
+    DVM_CUDA(cudaGetLastError());
+    return DVM_OK;
+}
+
 }  // namespace dvm
 
 using namespace dvm;
@@ -185,42 +225,6 @@ dvm_status_t dvm_ipc_open(const unsigned char handle[64], void **out)
 dvm_status_t dvm_ipc_close(void *dptr)
 {
     if (dptr) DVM_CUDA(cudaIpcCloseMemHandle(dptr));
-    return DVM_OK;
-}
-
-dvm_status_t dvm_collide_push(dvm_plan_t P, const double *f, int64_t ncells, void *const *windows, int rank,
-                              int world, unsigned int epoch)
-{
-    if (!P || !f || !windows) {
-        set_error("NULL argument");
-        return DVM_E_NULL;
-    }
-    dvm_status_t st = check_peer(P, ncells, world);
-    if (st) return st;
-    if (rank != P->shard_rank || epoch == 0) {
-        set_error(epoch == 0 ? "epoch must be >= 1" : "rank must equal the plan's shard_rank");
-        return DVM_E_STATE;
-    }
-    for (int r = 0; r < world; ++r)
-        if (!windows[r]) {
-            set_error("NULL peer window");
-            return DVM_E_NULL;
-        }
-    const int64_t n = ncells * nodes_per_cell(P);
-    const size_t cofs = slots_bytes(n, world);
-    double *mine = (double *)windows[rank] + (size_t)rank * n;
-    // Q_rank straight into the local slot
-    if ((st = collide_batched(P, f, mine, ncells, nodes_per_cell(P)))) return st;
-    PeerPtrs pp;
-    for (int r = 0; r < world; ++r) {
-        pp.slot[r] = (double2 *)((double *)windows[r] + (size_t)rank * n);
-        pp.ctr[r] = (unsigned int *)((char *)windows[r] + cofs) + rank;
-    }
-    {
-        LaunchScope ls(P, KC_REDUCE);
-        k_peer_push<<<push_blocks(n), kPeerThreads, 0, P->stream>>>((const double2 *)mine, n / 2, pp, world, rank);
-    }
-    DVM_CUDA(cudaGetLastError());
     return DVM_OK;
 }
 
