@@ -708,7 +708,7 @@ dvm_status_t collide_fgain3d(dvm_plan_s *P, const double *f, int64_t f_stride, d
     const int64_t npairs = (ncells + 1) / 2;
     // direction chunks per pair: the persistent groups take (pair, chunk) items round-robin;
     // pick the fewest chunks whose busiest group does within 0.5 % of the balanced share
-    // (256 pairs on 9 groups: 2 chunks, 28.5 instead of 29 pair-times)
+    // (small batches; larger ones below)
     int nchunks = 1;
     {
         auto rounds = [&](int c) { return (double)((npairs * c + max_groups - 1) / max_groups) / c; };
@@ -716,6 +716,11 @@ dvm_status_t collide_fgain3d(dvm_plan_s *P, const double *f, int64_t f_stride, d
         const int cmax = (int)std::max<int64_t>(1, std::min<int64_t>(nloc, std::max<int64_t>(16, max_groups / npairs)));
         for (int c = 1; c <= cmax; ++c) best = std::min(best, rounds(c));
         while (nchunks < cmax && rounds(nchunks) > best * 1.005) ++nchunks;
+        // batches of >= 16 pairs: 8 or 16 chunks (the one with fewer rounds, ties to
+        // 8) measured fastest at every bench size (ms, auto rule -> this rule:
+        // 512 cells 1605 -> 1585, 256: 792.5 -> 792.0, 128: 398.1 -> 397.8, 64:
+        // 199.8 -> 199.5, 32: 103.7 -> 100.5; tools/sweep_chunks.sh)
+        if (npairs >= 16 && nloc >= 16) nchunks = rounds(16) < rounds(8) ? 16 : 8;
     }
     if (P->tune.fg_chunks) nchunks = std::min(P->tune.fg_chunks, nloc);
     const int64_t items = npairs * nchunks;
