@@ -720,7 +720,12 @@ dvm_status_t collide_fgain3d(dvm_plan_s *P, const double *f, int64_t f_stride, d
         // 8) measured fastest at every bench size (ms, auto rule -> this rule:
         // 512 cells 1605 -> 1585, 256: 792.5 -> 792.0, 128: 398.1 -> 397.8, 64:
         // 199.8 -> 199.5, 32: 103.7 -> 100.5; tools/sweep_chunks.sh)
-        if (npairs >= 16 && nloc >= 16) nchunks = rounds(16) < rounds(8) ? 16 : 8;
+        if (npairs >= 16 && nloc >= 16) {
+            const int c = rounds(16) < rounds(8) ? 16 : 8;
+            // the chunk partials take c x the batch's Q: keep them under 24 GB (huge
+            // batches keep the balance rule's fewer chunks)
+            if ((double)c * (double)npairs * (double)FNODES * sizeof(double2) <= 24e9) nchunks = std::max(nchunks, c);
+        }
     }
     if (P->tune.fg_chunks) nchunks = std::min(P->tune.fg_chunks, nloc);
     const int64_t items = npairs * nchunks;
