@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(256) k_small2d_sum_euler(const double *__restr
 // G stays in a register; Q := −fΛ + G.  No scratch, no per-unit partials.
 // c3: 0.123 ms (the line-walk kernels + partial sum: 0.194 ms); bound by the
 // shared-memory loads (Σ_e (2M_e + 1) = 4568 per node for c3) with 16 warps per SM.
-constexpr int kTile = 16;             // tile rows
+constexpr int kTile = 16;             // tile rows (at most; a launch may use fewer, see collide_tiles)
 constexpr int kTileC = TILE2D_COLS;    // tile columns (one warp per row)
 
 // the tile kernel's body; getU(u) returns unit u (shared memory, or the kernel
@@ -384,12 +384,12 @@ constexpr int kTileC = TILE2D_COLS;    // tile columns (one warp per row)
 // instead of shared-memory wavefronts)
 template <class GetU>
 __device__ __forceinline__ void tile2d_body(const double *__restrict__ f, int64_t f_stride, int nunits, int N, int H,
-                                            double *__restrict__ Q, int64_t q_stride, double *s2, GetU getU)
+                                            double *__restrict__ Q, int64_t q_stride, double *s2, int R, GetU getU)
 {
-    const int PR = kTile + 2 * H, P = kTileC + 2 * H;  // rows, pitch of the tile + halo
+    const int PR = R + 2 * H, P = kTileC + 2 * H;  // rows, pitch of the tile + halo (R tile rows)
     const int t = threadIdx.x;
     const int64_t cell = blockIdx.z;
-    const int r0 = blockIdx.y * kTile, c0 = blockIdx.x * kTileC;
+    const int r0 = blockIdx.y * R, c0 = blockIdx.x * kTileC;
     const double *fc = f + cell * f_stride;
     for (int i = t; i < PR * P; i += blockDim.x) {
         const int rr = i / P, cc = i - rr * P;
@@ -398,6 +398,7 @@ __device__ __forceinline__ void tile2d_body(const double *__restrict__ f, int64_
     }
     __syncthreads();
     const int ty = t / kTileC, tx = t % kTileC;
+    if (r0 + ty >= N) return;  // rows past the grid in the last, ragged row of tiles
     const double *c = s2 + (H + ty) * P + (H + tx);
     const double fx = c[0];
     double g = 0.0;
@@ -434,13 +435,13 @@ __device__ __forceinline__ void tile2d_body(const double *__restrict__ f, int64_
 
 __global__ void __launch_bounds__(kTile * kTileC) k_tile2d(const double *__restrict__ f, int64_t f_stride,
                                                 const Unit2D *__restrict__ units, int nunits, int N, int H,
-                                                double *__restrict__ Q, int64_t q_stride)
+                                                double *__restrict__ Q, int64_t q_stride, int R)
 {
     extern __shared__ __align__(16) double s2[];
-    const int PR = kTile + 2 * H, P = kTileC + 2 * H;
+    const int PR = R + 2 * H, P = kTileC + 2 * H;
     Unit2D *su = reinterpret_cast<Unit2D *>(s2 + ((PR * P + 1) & ~1));
     for (int i = threadIdx.x; i < nunits; i += blockDim.x) su[i] = units[i];
-    tile2d_body(f, f_stride, nunits, N, H, Q, q_stride, s2, [&](int u) { return su[u]; });
+    tile2d_body(f, f_stride, nunits, N, H, Q, q_stride, s2, R, [&](int u) { return su[u]; });
 }
 
 constexpr int kParamUnits = 256;
@@ -450,17 +451,17 @@ struct TileUnits {
 
 __global__ void __launch_bounds__(kTile * kTileC) k_tile2d_pu(const double *__restrict__ f, int64_t f_stride,
                                                    int nunits, int N, int H, double *__restrict__ Q,
-                                                   int64_t q_stride, const __grid_constant__ TileUnits pu)
+                                                   int64_t q_stride, int R, const __grid_constant__ TileUnits pu)
 {
     extern __shared__ __align__(16) double s2[];
-    tile2d_body(f, f_stride, nunits, N, H, Q, q_stride, s2, [&](int u) { return pu.u[u]; });
+    tile2d_body(f, f_stride, nunits, N, H, Q, q_stride, s2, R, [&](int u) { return pu.u[u]; });
 }
 
 }  // namespace
 
-size_t tile2d_smem(int Ntilde, int nunits)
+size_t tile2d_smem(int Ntilde, int nunits, int R = kTile)
 {
-    const int PR = kTile + 2 * Ntilde, P = kTileC + 2 * Ntilde;
+    const int PR = R + 2 * Ntilde, P = kTileC + 2 * Ntilde;
     return sizeof(double) * (size_t)((PR * P + 1) & ~1) + sizeof(Unit2D) * (size_t)nunits;
 }
 
@@ -665,8 +666,23 @@ dvm_status_t collide_pair2d(dvm_plan_s *P, const double *f, int64_t f_stride, do
     if (nunits == 0) return DVM_OK;
     // the tile kernel when its tile + halo fits shared memory and the batch has enough
     // tiles for most SMs (c3: 128 tiles; dvm_set_path 7 forces it, 2 the line walks)
-    const size_t tsm = tile2d_smem(P->Ntilde, nunits);
     const int64_t ntiles = (int64_t)(N / kTileC) * (N / kTile) * ncells;
+    // tile rows R <= 16 minimising (waves of CTAs) x R: c3 (one 256^2 grid) takes
+    // R = 15, 18 x 8 = 144 CTAs in one wave instead of 128 of 16 rows (the last
+    // row of tiles ragged); ties keep 16
+    int R = kTile;
+    {
+        int sms = 148, dev = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        auto cost = [&](int r) {
+            const int64_t tl = (int64_t)(N / kTileC) * ((N + r - 1) / r) * ncells;
+            return ((tl + sms - 1) / sms) * r;
+        };
+        for (int r = kTile - 1; r >= 8; --r)
+            if (cost(r) < cost(R)) R = r;
+    }
+    const size_t tsm = tile2d_smem(P->Ntilde, nunits, R);
+    const unsigned tile_rows = (unsigned)((N + R - 1) / R);
     const bool tile = P->path_mode != 2 && N >= kTileC && tsm <= 227u * 1024u &&
                       (P->path_mode == 7 || ntiles >= 96);
     if (tile) {
@@ -689,12 +705,12 @@ dvm_status_t collide_pair2d(dvm_plan_s *P, const double *f, int64_t f_stride, do
             if (nunits <= kParamUnits && (int)P->g.h_units2d.size() == nunits * (int)sizeof(Unit2D)) {
                 TileUnits pu;
                 std::memcpy(pu.u, P->g.h_units2d.data(), sizeof(Unit2D) * (size_t)nunits);
-                k_tile2d_pu<<<dim3(N / kTileC, N / kTile, nc), kTile * kTileC, tsm, P->stream>>>(
-                    f + c0 * f_stride, f_stride, nunits, N, P->Ntilde, Q + c0 * q_stride, q_stride, pu);
+                k_tile2d_pu<<<dim3(N / kTileC, tile_rows, nc), R * kTileC, tsm, P->stream>>>(
+                    f + c0 * f_stride, f_stride, nunits, N, P->Ntilde, Q + c0 * q_stride, q_stride, R, pu);
             } else {
-                k_tile2d<<<dim3(N / kTileC, N / kTile, nc), kTile * kTileC, tsm, P->stream>>>(
+                k_tile2d<<<dim3(N / kTileC, tile_rows, nc), R * kTileC, tsm, P->stream>>>(
                     f + c0 * f_stride, f_stride, reinterpret_cast<const Unit2D *>(P->g.units), nunits, N, P->Ntilde,
-                    Q + c0 * q_stride, q_stride);
+                    Q + c0 * q_stride, q_stride, R);
             }
             DVM_CUDA(cudaGetLastError());
         }
